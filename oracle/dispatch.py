@@ -1,0 +1,103 @@
+"""Count exchange (a0) and replica-balanced dispatch (a2).  Test infrastructure only.
+
+a0 -- PAPER.md:687-689 (step 1): "aggregate the number of tokens assigned to
+each expert class, via an all-reduce".  Reading A6: a token counts once per
+selected expert, i.e. popularity counts (token, expert) PAIRS.  cnt[g][e] is
+rank g's count; C_e = sum_g cnt[g][e].
+
+a2 -- PAPER.md:690-692 (step 2): "load-balances the tokens for a given expert
+class across its replicated instances"; per-replica capacity scales with r_e
+(PAPER.md:893-898).  Reading A8 fixes WHICH replica gets which pair:
+
+  * pairs are taken in global order (rank g, token t, choice j) -- with A21 that
+    is global token order;
+  * R = rank of the pair among all pairs of its expert e in that order
+    (a stable sort by expert);
+  * q = C_e div r_e, m = C_e mod r_e; the first m replicas take q+1 pairs, the
+    rest q, in contiguous chunks:
+        rho = R div (q+1)                      if R < m (q+1)
+              m + (R - m (q+1)) div q          otherwise
+        off = R - (rho q + min(rho, m));  slot = first_slot[e] + rho
+  * slot_load[first_slot[e] + rho] = q + (rho < m).
+
+Per-rank outputs (rank g's local pair index p = t*k + j):
+  dest_slot[p], dest_off[p]   -- where the pair goes
+  send_pair / send_gate      -- local pairs ordered by (slot, off) (slot-major)
+  send_count[j]              -- local pairs going to global slot j
+Reading A9: drop-free (no capacity), so every pair is placed.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def validate_ids(ids: np.ndarray, E: int) -> None:
+    if ids.size and (ids.min() < 0 or ids.max() >= E):
+        raise ValueError("MOE_ERR_DATA: expert id outside [0, E)")
+    if ids.ndim == 2 and ids.shape[1] > 1:
+        s = np.sort(ids, axis=1)
+        if (s[:, 1:] == s[:, :-1]).any():
+            raise ValueError("MOE_ERR_DATA: repeated expert within a token")
+
+
+def counts(ids_per_rank, E: int) -> np.ndarray:
+    """cnt[G][E] (int64): per-rank pair counts of each expert (a0)."""
+    out = np.zeros((len(ids_per_rank), E), dtype=np.int64)
+    for g, ids in enumerate(ids_per_rank):
+        flat = np.asarray(ids).reshape(-1)
+        for e in range(E):
+            out[g, e] = int(np.count_nonzero(flat == e))
+    return out
+
+
+def dispatch(ids_per_rank, gates_per_rank, first_slot, E: int) -> dict:
+    """Replica-balanced dispatch of all ranks' pairs under a contiguous plan."""
+    G = len(ids_per_rank)
+    for ids in ids_per_rank:
+        validate_ids(np.asarray(ids), E)
+    fs = np.asarray(first_slot, dtype=np.int64)
+    r = np.diff(fs)
+    GS = int(fs[-1])
+    cnt = counts(ids_per_rank, E)
+    C = cnt.sum(axis=0)
+
+    flat = [np.asarray(ids, dtype=np.int64).reshape(-1) for ids in ids_per_rank]
+    glob = np.concatenate(flat) if flat else np.zeros(0, dtype=np.int64)
+
+    # R: rank of each pair within its expert, in global (g, t, j) order
+    R = np.empty(glob.size, dtype=np.int64)
+    for e in range(E):
+        where = np.nonzero(glob == e)[0]          # ascending global positions
+        R[where] = np.arange(where.size)
+
+    q = C // r
+    m = C % r
+    qe, me = q[glob], m[glob]
+    first_branch = R < me * (qe + 1)
+    rho = np.where(first_branch, R // (qe + 1),
+                   me + (R - me * (qe + 1)) // np.maximum(qe, 1))
+    off = R - (rho * qe + np.minimum(rho, me))
+    slot = fs[glob] + rho
+
+    slot_load = np.zeros(GS, dtype=np.int64)
+    for e in range(E):
+        for p in range(int(r[e])):
+            slot_load[fs[e] + p] = q[e] + (1 if p < m[e] else 0)
+
+    out = {"cnt": cnt, "C": C, "slot_load": slot_load, "ranks": []}
+    base = 0
+    for g in range(G):
+        n = flat[g].size
+        ds = slot[base:base + n]
+        do = off[base:base + n]
+        order = np.lexsort((do, ds))            # by slot, then offset
+        gates = np.asarray(gates_per_rank[g], dtype=np.float32).reshape(-1)
+        out["ranks"].append({
+            "dest_slot": ds.astype(np.int32),
+            "dest_off": do.astype(np.int32),
+            "send_pair": order.astype(np.int32),
+            "send_gate": gates[order],
+            "send_count": np.bincount(ds, minlength=GS).astype(np.int32),
+        })
+        base += n
+    return out
