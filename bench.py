@@ -1,0 +1,378 @@
+#!/usr/bin/env python
+"""Benchmark of the decoupled-MoE expert step (BASELINE.json metric:
+"decoupled expert step ms/iter + % of HBM/NVLink roofline at 1/2/4/8 B200").
+
+One step = one pass of the whole hot path over one iteration of a
+synthetic routing trace: a0 count exchange + a2 dispatch (device) -> a1 Alg. 1 plan for t+1
+(host C++, overlapping the scatter) -> a3 reduce + a4 Adam + a5 place (one fused kernel).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config gpt-small] [--impl reference]
+
+N = 1: the GPT-MoE-small workload (BASELINE.json configs[1]) with all 64 slots on one GPU.
+N > 1 (torchrun, one process per GPU): the same workload, S*G = 64 fixed (strong scaling);
+real mode with CUDA-IPC peer mappings over NVLink.  Timing: W warm-up steps, then exactly K
+steps between barrier + synchronize, CUDA events on the launching stream, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+GUIDE_NVLINK_GBS = 770.0      # measured peer copy per direction (B200_PROFILING.md)
+FALLBACK_HBM_GBS = 6650.0     # B200_PROFILING.md fallback if MEASURED_PEAKS.json is absent
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)", float(d.get("sm_max_mhz", 0))
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)", 0.0
+
+
+def _env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.idx), "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+def algorithmic_bytes(wl, G: int, S: int) -> dict:
+    """per GPU per iteration."""
+    P, E = wl.P, wl.E
+    Pg = P // G
+    pairs = (wl.T // G) * wl.k
+    upd_hbm = 2 * S * P + 24 * E * Pg + 2 * S * P       # grads read + master/m/v rw + weights written
+    nvl_dir = 2 * (2 * S * (G - 1) * P // G)             # reduce pulls + place pushes, per direction
+    return {"dispatch_hbm": 28 * pairs, "update_hbm": upd_hbm, "update_nvlink_per_dir": nvl_dir}
+
+
+# ------------------------------------------------------------------------------------------
+# reference arm / cpu_baseline: the oracle as it stands, on a bounded sample
+# ------------------------------------------------------------------------------------------
+def run_oracle_sample(wl, G: int, iters: int, frac_den: int = 256, seed_shift: int = 0):
+    """Times OracleSim on the SAME workload: full count exchange + dispatch + plan for all
+    T*k pairs, and reduce/Adam/place on 1/frac_den of every expert's elements (stride
+    sample), extrapolated x frac_den (every stage after dispatch is elementwise per expert).
+    Returns (ms per full iteration, description, per-iteration seconds)."""
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    from oracle import dispatch as od
+    from oracle import plan as op
+    from oracle import step as ostep
+    from synth import configs, hashgen, traces
+    S = wl.S(G)
+    seed = configs.seed_for(wl.name) + seed_shift
+    idx = np.arange(0, wl.P, frac_den, dtype=np.int64)
+    sim = ostep.OracleSim(wl.E, G, S, wl.P, seed, idx=idx)
+    tr = traces.make_trace(wl, iters=iters)
+    per = []
+    for t, (ids, gates) in enumerate(tr):
+        ids_r, gates_r = traces.split_ranks(ids, G), traces.split_ranks(gates, G)
+        grads = {j: hashgen.grad_bits(seed, t, j, idx.astype(np.uint64)) for j in range(G * S)}
+        t0 = time.perf_counter()
+        disp = od.dispatch(ids_r, gates_r, sim.plan["first_slot"], wl.E)     # a0 + a2 (full)
+        op.plan(disp["C"], wl.E, G, S)                                     # a1 (full)
+        t1 = time.perf_counter()
+        sim.iterate(ids_r, gates_r, lambda j: grads[j])                    # a0..a5 (sampled elems)
+        t2 = time.perf_counter()
+        # sim.iterate repeats dispatch + plan on the full pair set: subtract that share
+        elementwise = max(0.0, (t2 - t1) - (t1 - t0))
+        per.append((t1 - t0) + elementwise * frac_den)
+    desc = (f"{wl.name} G={G}: full a0/a1/a2 on all {wl.T * wl.k} pairs; a3-a5 on every "
+            f"{frac_den}th element of all {wl.E} experts x {G * S} slots, extrapolated x{frac_den}")
+    return 1000.0 * statistics.median(per), desc, per
+
+
+def reference_arm(args, wl):
+    rank, world, _ = _env_rank()
+    if rank != 0:
+        return 0
+    import numpy as _np  # noqa: F401
+    G = args.gpus
+    total = args.warmup + args.steps
+    t0 = time.perf_counter()
+    ms, desc, per = run_oracle_sample(wl, G, total, frac_den=args.ref_frac)
+    timed = per[args.warmup:] if len(per) > args.warmup else per
+    val = 1000.0 * statistics.median(timed)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(val, 3), "unit": "ms/iter",
+        "n_gpus": G, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(val, 3),
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": _config(wl, G),
+        "cpu_baseline": {"value": round(val, 3), "unit": "ms/iter", "cores": 1, "kind": "oracle",
+                         "sample": desc},
+        "e2e": {"value": round(val, 3), "unit": "ms/iter", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "wall_s": round(time.perf_counter() - t0, 1),
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+METRIC = "decoupled expert step ms/iter + % of HBM/NVLink roofline at 1/2/4/8 B200"
+
+
+def _config(wl, G):
+    return {"workload": wl.name, "E": wl.E, "d": wl.d, "ffn": wl.ffn, "P": wl.P, "k": wl.k,
+            "T": wl.T, "G": G, "S": wl.S(G), "trace": wl.trace,
+            "parallelism": f"decoupled-ep{G}",
+            "l2": "inputs larger than L2 (optimizer state + slot grads/weights stream >126 MB per step)"}
+
+
+# ------------------------------------------------------------------------------------------
+# GPU arm
+# ------------------------------------------------------------------------------------------
+def gpu_arm(args, wl):
+    import torch
+    import torch.distributed as dist
+    rank, world, local = _env_rank()
+    G = args.gpus
+    if world != G:
+        raise SystemExit(f"--gpus {G} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if G > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import __graft_entry__
+    if rank == 0:
+        __graft_entry__.build()
+    if G > 1:
+        dist.barrier()
+    from paper_2504_19925_b200 import DecoupledExpertLayer, api
+    from synth import configs, traces
+
+    S = wl.S(G)
+    Tg = wl.tokens_per_rank(G)
+    seed = configs.seed_for(wl.name)
+    layer = DecoupledExpertLayer(wl.E, G, S, wl.k, wl.P, Tg, rank=rank if G > 1 else 0,
+                                 device=local, seed=seed)
+    if G > 1:
+        layer.connect()
+    n_tr = min(args.warmup + args.steps, args.trace_iters)
+    tr = traces.make_trace(wl, iters=n_tr)
+    ids_d = [torch.from_numpy(traces.split_ranks(i, G)[rank].copy()).cuda() for i, _ in tr]
+    gates_d = [torch.from_numpy(traces.split_ranks(g, G)[rank].copy()).cuda() for _, g in tr]
+    api.synth_grads(layer.slot_g[0], seed, 0, rank * S, S, wl.P)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if G > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream()
+
+    def step(i, ev=None):
+        t = i % n_tr
+        if ev is not None:
+            ev[0].record(stream)
+        layer.dispatch(ids_d[t], gates_d[t], Tg)
+        if ev is not None:
+            ev[1].record(stream)
+        h0 = time.perf_counter()
+        nxt = layer.plan_next()
+        h1 = time.perf_counter()
+        if ev is not None:
+            ev[2].record(stream)
+        layer.update(nxt)
+        if ev is not None:
+            ev[3].record(stream)
+        return h1 - h0
+
+    for i in range(args.warmup):
+        step(i)
+    layer.ctx.check()
+    K = args.steps
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clk = ClockSampler(local)
+    barrier()
+    clk.start()
+    time.sleep(0.3)
+    barrier()
+    start.record(stream)
+    plan_s = []
+    for i in range(K):
+        plan_s.append(step(args.warmup + i, evs[i]))
+    end.record(stream)
+    barrier()
+    clocks = clk.stop()
+    layer.ctx.check()
+    total_ms = start.elapsed_time(end)
+    disp_ms = [e[0].elapsed_time(e[1]) for e in evs]
+    upd_ms = [e[2].elapsed_time(e[3]) for e in evs]
+    t = torch.tensor([total_ms, statistics.mean(upd_ms), statistics.mean(disp_ms)], device="cuda")
+    if G > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, upd_avg, disp_avg = (float(x) for x in t.tolist())
+    ms_iter = total_ms / K
+
+    # ---- e2e: the same steps through the public API with HOST buffers (pinned) ----------
+    e2e = None
+    if not args.no_e2e:
+        ids_h = [x.cpu().pin_memory() for x in ids_d]
+        gates_h = [x.cpu().pin_memory() for x in gates_d]
+        grads_h = layer.slot_g[0].cpu().pin_memory()
+        ids_buf = torch.empty_like(ids_d[0])
+        gates_buf = torch.empty_like(gates_d[0])
+        Ke = max(3, min(K, args.e2e_steps))
+        barrier()
+        s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s2.record(stream)
+        for i in range(Ke):
+            tt = i % n_tr
+            ids_buf.copy_(ids_h[tt], non_blocking=True)
+            gates_buf.copy_(gates_h[tt], non_blocking=True)
+            layer.slot_g[0].copy_(grads_h, non_blocking=True)
+            layer.iterate(ids_buf, gates_buf, Tg)       # counts come back to pinned host inside
+        e2.record(stream)
+        barrier()
+        et = torch.tensor([s2.elapsed_time(e2) / Ke], device="cuda")
+        if G > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e = {"value": round(float(et.item()), 4), "unit": "ms/iter",
+               "h2d_bytes_per_step": int(ids_buf.numel() * 4 + gates_buf.numel() * 4 + grads_h.numel() * 2),
+               "d2h_bytes_per_step": int(wl.E * 8),
+               "note": "inputs per step: topk_ids + gates + all slot grads (bf16) from pinned host memory; "
+                       "result: C_e counts to pinned host"}
+        layer.ctx.check()
+
+    peak_hbm, peak_src, _ = _peaks()
+    ab = algorithmic_bytes(wl, G, S)
+    if G == 1:
+        achieved = ab["update_hbm"] / (upd_avg * 1e-3) / 1e9
+        roof = {"kernel": "k_update (fused reduce+Adam+place)", "bound": "hbm",
+                "achieved": round(achieved, 1), "peak": peak_hbm, "unit": "GB/s",
+                "frac": round(achieved / peak_hbm, 4), "traffic": args.traffic,
+                "algorithmic_bytes_per_launch": ab["update_hbm"], "peak_source": peak_src,
+                "avg_launch_ms": round(upd_avg, 4)}
+    else:
+        t_hbm = ab["update_hbm"] / (peak_hbm * 1e9)
+        t_nvl = ab["update_nvlink_per_dir"] / (GUIDE_NVLINK_GBS * 1e9)
+        if t_nvl >= t_hbm:
+            achieved = ab["update_nvlink_per_dir"] / (upd_avg * 1e-3) / 1e9
+            roof = {"kernel": "k_update (fused reduce+Adam+place, NVLink pulls/pushes)",
+                    "bound": "nvlink", "achieved": round(achieved, 1), "peak": GUIDE_NVLINK_GBS,
+                    "unit": "GB/s", "frac": round(achieved / GUIDE_NVLINK_GBS, 4), "traffic": None,
+                    "algorithmic_bytes_per_launch": ab["update_nvlink_per_dir"],
+                    "peak_source": "B200_PROFILING.md measured peer copy per direction (900 nominal)",
+                    "avg_launch_ms": round(upd_avg, 4)}
+        else:
+            achieved = ab["update_hbm"] / (upd_avg * 1e-3) / 1e9
+            roof = {"kernel": "k_update", "bound": "hbm", "achieved": round(achieved, 1),
+                    "peak": peak_hbm, "unit": "GB/s", "frac": round(achieved / peak_hbm, 4),
+                    "traffic": None, "algorithmic_bytes_per_launch": ab["update_hbm"],
+                    "peak_source": peak_src, "avg_launch_ms": round(upd_avg, 4)}
+    t_roof_step = max((ab["update_hbm"] + ab["dispatch_hbm"]) / (peak_hbm * 1e9),
+                      ab["update_nvlink_per_dir"] / (GUIDE_NVLINK_GBS * 1e9) if G > 1 else 0.0)
+    launches_per_step = 3 + 1 + (2 if G > 1 else 0)
+
+    cpu = None
+    if rank == 0 and G == 1 and not args.no_cpu_baseline:
+        ms, desc, _ = run_oracle_sample(wl, G, args.cpu_iters, frac_den=args.cpu_frac)
+        cpu = {"value": round(ms, 1), "unit": "ms/iter", "cores": 1, "kind": "oracle", "sample": desc}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(ms_iter, 4), "unit": "ms/iter", "n_gpus": G,
+            "steps": K, "warmup": args.warmup, "ms_per_step": round(ms_iter, 4),
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic (walk-spike routing trace, counter-hash grads)",
+            "config": _config(wl, G),
+            "roofline": roof,
+            "step_roofline": {"t_roof_ms": round(t_roof_step * 1e3, 4),
+                              "frac": round(t_roof_step * 1e3 / ms_iter, 4),
+                              "basis": "max(HBM bytes of dispatch+update / peak HBM, NVLink bytes/dir / 770 GB/s)"},
+            "stages_ms": {"dispatch": round(disp_avg, 4), "update": round(upd_avg, 4),
+                          "host_plan_wait": round(1e3 * statistics.mean(plan_s), 4)},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * K,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    layer.close()
+    if G > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="gpt-small")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--trace-iters", type=int, default=25)
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-iters", type=int, default=3)
+    ap.add_argument("--cpu-frac", type=int, default=64)
+    ap.add_argument("--ref-frac", type=int, default=256)
+    ap.add_argument("--traffic", type=float, default=None,
+                    help="dram bytes per k_update launch from an ncu --set full capture")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 0)
+    from synth import configs
+    wl = configs.CONFIGS[args.config]
+    if args.impl == "reference":
+        return reference_arm(args, wl)
+    return gpu_arm(args, wl)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

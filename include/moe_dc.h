@@ -1,0 +1,212 @@
+/*
+ * moe_dc.h -- C ABI of the B200-native decoupled-MoE expert step
+ *             (arXiv 2504.19925, "Efficient Mixture-of-Experts Training via
+ *             Model and Optimizer State Decoupling").
+ *
+ * One MoE layer, one training iteration t, five stages:
+ *
+ *   a0 count exchange  PAPER.md:687-689 (fig:design_diagram step 1): every
+ *                      rank's per-expert (token, expert) pair counts are
+ *                      exchanged; C_e = sum over ranks.        -> moe_dispatch
+ *   a1 plan            PAPER.md:1519-1564 (Alg. 1, apx:algo_scheduler),
+ *                      912-923 (sec:design_sched): C -> replica counts r_e and
+ *                      a contiguous slot map, used at iteration t+1. -> moe_plan
+ *   a2 dispatch        PAPER.md:690-692 (step 2): pairs of expert e are split
+ *                      evenly over e's r_e replicas.           -> moe_dispatch
+ *   a3 reduce          PAPER.md:965-969 (sec:comm_allreduce), 747-748: the
+ *                      replicas' grads are summed onto the owners' static
+ *                      optimizer shards.                        -> moe_update
+ *   a4 update          PAPER.md:705-708 (steps 4-5), 1600-1625 (apx:nonoffload):
+ *                      fused Adam on each owner's fp32 shard.    -> moe_update
+ *   a5 place           PAPER.md:711, 743, 997-1001 (step 8, sec:comm_scatweights):
+ *                      updated bf16 shards are written straight into the slots
+ *                      of the NEXT placement (no separate migration). -> moe_update
+ *
+ * Conventions (every function):
+ *   - Returns an int status (moe_status); 0 == MOE_OK.  No C++ exception ever
+ *     crosses this boundary.  On failure moe_last_error() gives a thread-local
+ *     message.
+ *   - Sizes are element counts unless named *_bytes.
+ *   - "stream" is a cudaStream_t passed as void*; device work is enqueued on it
+ *     and the call returns without synchronising (except where stated).
+ *   - All tensors are caller-owned (PyTorch allocates them).  The library owns
+ *     only the context: scratch sized at creation, the cross-GPU sync buffer,
+ *     and the peer mappings.  Caller buffers must stay alive until the stream
+ *     work that uses them has completed.
+ *   - Notation: E experts, G GPUs (the paper's N), S slots per GPU (the paper's
+ *     s), P parameters per expert, k top-k, T tokens per rank, Pg = P / G.
+ *   - Global slot j lives on GPU j / S at local slot j % S.
+ *   - Optimizer shards: GPU g owns elements [g*Pg, (g+1)*Pg) of EVERY expert
+ *     ("uniformly partitions each expert's optimizer across all N
+ *     nodes"; optimal per apx:opt_part).  They never move.
+ */
+#ifndef MOE_DC_H
+#define MOE_DC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MOE_ABI_VERSION 1
+#define MOE_MAX_E 256     /* experts per layer                              */
+#define MOE_MAX_G 8       /* GPUs: one NVSwitch box                         */
+#define MOE_MAX_SLOTS 4096 /* G*S                                           */
+
+typedef enum {
+  MOE_OK = 0,
+  MOE_ERR_INVALID = 1,  /* bad argument: E<1, G<1, S<1, E>G*S, k<1, k>E,
+                           T<0 or T>max_tokens, NULL pointer, negative count, limits  */
+  MOE_ERR_SHAPE = 2,    /* plan E/G/S differ from the context, or a plan is not a
+                           valid contiguous placement (SPEC.md:141 ShapeMismatch)     */
+  MOE_ERR_DATA = 3,     /* device data invalid: a topk id outside [0,E) or repeated
+                           within a token.  Raised by a device flag, reported by
+                           moe_ctx_check().  Outputs of that call are undefined.     */
+  MOE_ERR_CUDA = 4,     /* CUDA runtime failure                                     */
+  MOE_ERR_COMM = 5,     /* peer mapping (CUDA IPC) failure                          */
+  MOE_ERR_INTERNAL = 6, /* library invariant violated                               */
+  MOE_ERR_TIMEOUT = 7   /* a cross-GPU flag wait exceeded its timeout (a peer never
+                           arrived); reported by moe_ctx_check()                    */
+} moe_status;
+
+const char *moe_status_str(int status);
+const char *moe_last_error(void);
+int moe_abi_version(void);
+
+/* ------------------------------------------------------------------------------------------
+ * a1 Plan -- host only, synchronous, pure, thread-safe; no CUDA.
+ *
+ * moe_plan_t holds a placement.  All arrays are caller-allocated host memory:
+ *   replicas    [E]     r_e >= 1, sum == G*S                 (Eq. (2), 919)
+ *   first_slot  [E+1]   exclusive prefix of replicas; first_slot[E] == G*S
+ *   slot_expert [G*S]   global slot -> expert, non-decreasing (contiguous)
+ * ------------------------------------------------------------------------------------------ */
+typedef struct {
+  int32_t E, G, S;
+  int32_t *replicas;
+  int32_t *first_slot;
+  int32_t *slot_expert;
+} moe_plan_t;
+
+typedef enum {
+  MOE_PLAN_PAPER_ALG1 = 0, /* Alg. 1 exactly (readings A2-A5) */
+  MOE_PLAN_MINMAX = 1      /* greedy Adams apportionment: minimises max C_e / r_e
+                              (reading A1)                                        */
+} moe_plan_policy;
+
+/* counts: [E] global pair counts C_e >= 0 (host).  sum == 0 means uniform (reading A3).
+ * Writes out->replicas, out->first_slot, out->slot_expert and sets out->E/G/S.
+ * Errors: MOE_ERR_INVALID (E<1, G<1, slots<1, E>G*slots, E>MOE_MAX_E,
+ * G*slots>MOE_MAX_SLOTS, a NULL pointer, a negative count).                      */
+int moe_plan(const int64_t *counts, int32_t E, int32_t G, int32_t slots, moe_plan_t *out);
+
+/* As moe_plan with an explicit policy.  steps (nullable, [2]) receives the number of
+ * over- and under-allocation correction steps of Alg. 1 (0 for MINMAX).           */
+int moe_plan_ex(const int64_t *counts, int32_t E, int32_t G, int32_t slots, int32_t policy,
+                moe_plan_t *out, int64_t *steps);
+
+/* ------------------------------------------------------------------------------------------
+ * Context: binds the persistent, peer-visible buffers of one GPU (real mode) or of all G
+ * simulated GPUs on one device (virtual mode, rank = -1).
+ * ------------------------------------------------------------------------------------------ */
+typedef struct moe_ctx moe_ctx;
+
+typedef struct {
+  int32_t E, G, S, k;
+  int64_t P;            /* params per expert; P % G == 0 and (P / G) % 8 == 0 (pad with zeros;
+                           DESIGN.md reading A12)                                        */
+  int64_t max_tokens;   /* per-rank token upper bound; sizes the dispatch scratch        */
+  int32_t rank;         /* this process's GPU in [0, G), or -1 = virtual mode (all G
+                           ranks on this one device, n_local = G)                         */
+  int32_t device;       /* CUDA device ordinal                                            */
+  /* per local rank (1 pointer in real mode, G in virtual mode), caller-owned device memory: */
+  void *const *slot_w;   /* bf16 [S][P]   slot weights (written by moe_update's place)   */
+  void *const *slot_g;   /* bf16 [S][P]   slot gradients (read by moe_update's reduce)   */
+  float *const *master;  /* fp32 [E][Pg]  owner shard: master weights                    */
+  float *const *adam_m;  /* fp32 [E][Pg]  owner shard: first moment                      */
+  float *const *adam_v;  /* fp32 [E][Pg]  owner shard: second moment                     */
+} moe_ctx_desc;
+
+/* Creates a context (allocates scratch and the sync buffer on desc->device).
+ * Virtual mode is ready immediately.  Real mode (G > 1) additionally needs
+ * moe_ctx_export + an exchange of the handles between ranks + moe_ctx_connect.  */
+int moe_ctx_create(const moe_ctx_desc *desc, moe_ctx **out);
+int moe_ctx_destroy(moe_ctx *ctx);
+
+/* Bytes of this rank's peer-mapping record (CUDA IPC handles + offsets).        */
+int moe_ctx_handle_bytes(void);
+/* Writes this rank's record into out[moe_ctx_handle_bytes()] (host).            */
+int moe_ctx_export(moe_ctx *ctx, void *out);
+/* all: G records in rank order (host), as gathered by the caller's process group.
+ * Maps every peer's slot_g / slot_w / sync buffer.  Collective in spirit: every rank
+ * must connect before any rank's first moe_dispatch / moe_update.               */
+int moe_ctx_connect(moe_ctx *ctx, const void *all);
+
+/* Synchronises `stream`, then reports and clears device-raised errors
+ * (MOE_ERR_DATA, MOE_ERR_TIMEOUT).                                               */
+int moe_ctx_check(moe_ctx *ctx, void *stream);
+
+/* Blocks the calling host thread until the C_e copy of the most recent moe_dispatch
+ * has landed in out->counts_host (an event recorded right after that copy, BEFORE the
+ * scatter kernel), so the host planner (step 6 may "execute earlier, even right after
+ * step 1", PAPER.md:709 fn) overlaps the scatter.  MOE_OK if no dispatch was issued.  */
+int moe_ctx_wait_counts(moe_ctx *ctx);
+
+/* ------------------------------------------------------------------------------------------
+ * a0 + a2 Dispatch -- device, asynchronous on `stream`; collective across GPUs in real mode
+ * (one-sided NVLink stores of the [E] counts plus a flag; no NCCL).
+ *
+ * topk_ids [n_local][T][k] int32 (device), gates [n_local][T][k] fp32 (device): rank v's
+ * tokens (virtual mode: the G rank blocks back to back, reading A21).  plan: the CURRENT
+ * placement plan_t (host), which must be a valid contiguous placement for the context.
+ * Pair p = t*k + j of rank v, in global order (v, t, j) (reading A8): R = its rank among
+ * all pairs of its expert e; q = C_e / r_e, m = C_e % r_e; the first m replicas take q+1
+ * pairs, the rest q, in contiguous chunks.
+ * ------------------------------------------------------------------------------------------ */
+typedef struct {
+  int32_t *dest_slot;   /* [n_local][T*k] global slot of pair p                          */
+  int32_t *dest_off;    /* [n_local][T*k] offset of pair p inside that slot's buffer      */
+  int32_t *send_pair;   /* [n_local][T*k] local pair ids ordered by (slot, offset)        */
+  float *send_gate;     /* [n_local][T*k] gates in send_pair order (bit-exact copies)     */
+  int32_t *send_count;  /* [n_local][G*S] pairs this rank sends to each global slot       */
+  int32_t *slot_load;   /* [G*S] global load of each slot: q or q+1 (device)              */
+  int64_t *counts_dev;  /* [E] C_e (device, nullable)                                      */
+  int64_t *counts_host; /* [E] C_e (PINNED host, nullable): input of the next moe_plan;
+                           valid once the stream work enqueued by this call completes      */
+} moe_dispatch_out;
+
+int moe_dispatch(moe_ctx *ctx, const int32_t *topk_ids, const float *gates, int64_t T,
+                 const moe_plan_t *plan, const moe_dispatch_out *out, void *stream);
+
+/* ------------------------------------------------------------------------------------------
+ * a3 + a4 + a5 Update -- device, asynchronous; collective in real mode.  One fused kernel per
+ * GPU streams its owned elements of every expert: pull the r_e replica slices of the slot
+ * grads bound in the ctx (local HBM or peer HBM over NVLink), sum them in the two-level
+ * fp32 order (ascending local slots, then ascending GPU; reading A11), scale (A10), run Adam
+ * on the fp32 master/m/v shard (op order: DESIGN.md reading A15; IEEE fp32, no FMA), round
+ * to bf16 RNE and store into every slot j of plan_next hosting e, on any GPU.
+ * Cross-GPU barriers (flags in peer memory, release/acquire at system scope) order
+ * "grads ready" before the pulls and "all weights landed" before the call's stream work ends.
+ * ------------------------------------------------------------------------------------------ */
+typedef struct {
+  double lr, beta1, beta2, eps, weight_decay;  /* host doubles; rounded once to fp32 */
+  int64_t step;                                /* t >= 1, shared by all experts      */
+  int32_t scale_mode;   /* 0: 1/r_e (mean, default)  1: plain sum  2: scale[e]          */
+  const float *scale;   /* [E] host, mode 2 only                                      */
+} moe_adam_t;
+
+int moe_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *plan_next,
+               const moe_adam_t *adam, void *stream);
+
+/* a5 alone: writes bf16 RNE of the owners' current fp32 master shards into every slot of
+ * `plan`.  Used to materialise the initial placement plan_0 (and after a
+ * checkpoint restore); the per-iteration path places inside moe_update.  Collective in
+ * real mode.                                                                          */
+int moe_place(moe_ctx *ctx, const moe_plan_t *plan, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOE_DC_H */

@@ -1,0 +1,224 @@
+"""Python binding of the C ABI (include/moe_dc.h): same names, argument marshalling only.
+
+Every stage of the path runs in libmoedc's kernels (or, for moe_plan, its host C++).
+PyTorch supplies device memory, streams and the process group that exchanges the
+peer-mapping records; nothing here computes any part of the method.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from ._lib import MOE_PLAN_MINMAX, MOE_PLAN_PAPER_ALG1, MoeError, check  # noqa: F401
+
+
+def _stream_ptr(stream) -> C.c_void_p:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream)
+
+
+def _ptr(t: torch.Tensor | None) -> C.c_void_p:
+    return C.c_void_p(t.data_ptr() if t is not None else 0)
+
+
+class Plan:
+    """A placement (moe_plan_t): replicas [E], first_slot [E+1], slot_expert [G*S] (host)."""
+
+    def __init__(self, E: int, G: int, S: int):
+        self.E, self.G, self.S = E, G, S
+        self.replicas = np.zeros(E, dtype=np.int32)
+        self.first_slot = np.zeros(E + 1, dtype=np.int32)
+        self.slot_expert = np.zeros(G * S, dtype=np.int32)
+        self._c = L.MoePlanT(E, G, S,
+                             self.replicas.ctypes.data_as(C.POINTER(C.c_int32)),
+                             self.first_slot.ctypes.data_as(C.POINTER(C.c_int32)),
+                             self.slot_expert.ctypes.data_as(C.POINTER(C.c_int32)))
+
+    @property
+    def c(self) -> L.MoePlanT:
+        return self._c
+
+    @classmethod
+    def from_first_slot(cls, first_slot, G: int, S: int) -> "Plan":
+        fs = np.asarray(first_slot, dtype=np.int32)
+        p = cls(fs.size - 1, G, S)
+        p.first_slot[:] = fs
+        p.replicas[:] = np.diff(fs)
+        p.slot_expert[:] = np.repeat(np.arange(p.E, dtype=np.int32), p.replicas)
+        return p
+
+
+def moe_plan(counts, E: int, G: int, slots: int, policy: int = MOE_PLAN_PAPER_ALG1,
+             return_steps: bool = False):
+    """a1: Alg. 1 (or MINMAX) on the host C++ planner."""
+    c = np.ascontiguousarray(counts, dtype=np.int64)
+    if c.size != E:
+        raise ValueError("counts must have E entries")
+    p = Plan(E, G, slots)
+    steps = np.zeros(2, dtype=np.int64)
+    check(L.lib().moe_plan_ex(c.ctypes.data_as(C.POINTER(C.c_int64)), E, G, slots, policy,
+                              C.byref(p.c), steps.ctypes.data_as(C.POINTER(C.c_int64))), "moe_plan")
+    return (p, (int(steps[0]), int(steps[1]))) if return_steps else p
+
+
+class MoeContext:
+    """moe_ctx: binds slot weights/grads and the owner's optimizer shards (caller tensors).
+
+    Real mode: rank in [0, G), one local rank (lists of length 1).
+    Virtual mode: rank = -1, G local ranks on one device (lists of length G).
+    """
+
+    def __init__(self, E: int, G: int, S: int, k: int, P: int, max_tokens: int, rank: int,
+                 slot_w, slot_g, master, adam_m, adam_v, device: int | None = None):
+        n_local = G if rank < 0 else 1
+        for name, lst in (("slot_w", slot_w), ("slot_g", slot_g), ("master", master),
+                          ("adam_m", adam_m), ("adam_v", adam_v)):
+            if len(lst) != n_local:
+                raise ValueError(f"{name}: expected {n_local} tensors")
+            for t in lst:
+                if not (t.is_cuda and t.is_contiguous()):
+                    raise ValueError(f"{name}: tensors must be contiguous CUDA tensors")
+        for t in list(slot_w) + list(slot_g):
+            if t.dtype != torch.bfloat16 or t.numel() != S * P:
+                raise ValueError("slot_w/slot_g: bf16 [S][P]")
+        for t in list(master) + list(adam_m) + list(adam_v):
+            if t.dtype != torch.float32 or t.numel() != E * (P // G):
+                raise ValueError("master/adam_m/adam_v: fp32 [E][P/G]")
+        self.E, self.G, self.S, self.k, self.P = E, G, S, k, P
+        self.rank, self.n_local, self.max_tokens = rank, n_local, max_tokens
+        self.device = slot_w[0].device.index if device is None else device
+        self._keep = (slot_w, slot_g, master, adam_m, adam_v)
+
+        def arr(lst):
+            a = (C.c_void_p * n_local)(*[t.data_ptr() for t in lst])
+            return a
+        self._arrs = [arr(slot_w), arr(slot_g), arr(master), arr(adam_m), arr(adam_v)]
+        desc = L.MoeCtxDesc(E, G, S, k, P, max_tokens, rank, self.device,
+                            *[C.cast(a, C.POINTER(C.c_void_p)) for a in self._arrs])
+        h = C.c_void_p()
+        check(L.lib().moe_ctx_create(C.byref(desc), C.byref(h)), "moe_ctx_create")
+        self._h = h
+
+    @property
+    def handle(self) -> C.c_void_p:
+        if self._h is None:
+            raise RuntimeError("context destroyed")
+        return self._h
+
+    def export(self) -> bytes:
+        n = L.lib().moe_ctx_handle_bytes()
+        buf = C.create_string_buffer(n)
+        check(L.lib().moe_ctx_export(self.handle, buf), "moe_ctx_export")
+        return buf.raw
+
+    def connect(self, records: list[bytes]) -> None:
+        if len(records) != self.G:
+            raise ValueError("need one record per rank")
+        blob = b"".join(records)
+        buf = C.create_string_buffer(blob, len(blob))
+        check(L.lib().moe_ctx_connect(self.handle, buf), "moe_ctx_connect")
+
+    def connect_process_group(self, group=None) -> None:
+        """Exchange the CUDA-IPC records over a torch.distributed group and map the peers."""
+        import torch.distributed as dist
+        recs = [None] * self.G
+        dist.all_gather_object(recs, self.export(), group=group)
+        self.connect(recs)
+
+    def wait_counts(self) -> None:
+        """Host waits for the C_e copy of the last moe_dispatch (not for its scatter)."""
+        check(L.lib().moe_ctx_wait_counts(self.handle), "moe_ctx_wait_counts")
+
+    def check(self, stream=None) -> None:
+        check(L.lib().moe_ctx_check(self.handle, _stream_ptr(stream)), "moe_ctx_check")
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None:
+            L.lib().moe_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class DispatchBuffers:
+    """Caller-owned outputs of moe_dispatch (moe_dispatch_out)."""
+
+    def __init__(self, ctx: MoeContext, T: int, pinned_counts: bool = True):
+        dev = torch.device("cuda", ctx.device)
+        n = ctx.n_local * T * ctx.k
+        GS = ctx.G * ctx.S
+        self.T = T
+        self.dest_slot = torch.empty(n, dtype=torch.int32, device=dev)
+        self.dest_off = torch.empty(n, dtype=torch.int32, device=dev)
+        self.send_pair = torch.empty(n, dtype=torch.int32, device=dev)
+        self.send_gate = torch.empty(n, dtype=torch.float32, device=dev)
+        self.send_count = torch.empty(ctx.n_local * GS, dtype=torch.int32, device=dev)
+        self.slot_load = torch.empty(GS, dtype=torch.int32, device=dev)
+        self.counts_dev = torch.empty(ctx.E, dtype=torch.int64, device=dev)
+        self.counts_host = torch.zeros(ctx.E, dtype=torch.int64, pin_memory=pinned_counts)
+        self._c = L.MoeDispatchOut(*(t.data_ptr() for t in (
+            self.dest_slot, self.dest_off, self.send_pair, self.send_gate, self.send_count,
+            self.slot_load, self.counts_dev, self.counts_host)))
+
+    @property
+    def c(self) -> L.MoeDispatchOut:
+        return self._c
+
+
+def moe_dispatch(ctx: MoeContext, topk_ids: torch.Tensor, gates: torch.Tensor, T: int,
+                 plan: Plan, out: DispatchBuffers, stream=None) -> None:
+    """a0 + a2 on the device (asynchronous)."""
+    if topk_ids.dtype != torch.int32 or gates.dtype != torch.float32:
+        raise ValueError("topk_ids int32, gates fp32")
+    if topk_ids.numel() != ctx.n_local * T * ctx.k or gates.numel() != topk_ids.numel():
+        raise ValueError("topk_ids/gates must hold n_local*T*k elements")
+    if out.T < T:
+        raise ValueError("DispatchBuffers too small")
+    check(L.lib().moe_dispatch(ctx.handle, _ptr(topk_ids), _ptr(gates), T, C.byref(plan.c),
+                               C.byref(out.c), _stream_ptr(stream)), "moe_dispatch")
+
+
+@dataclass
+class AdamConfig:
+    lr: float = 1e-4
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    weight_decay: float = 0.0
+
+
+def moe_update(ctx: MoeContext, plan_cur: Plan, plan_next: Plan, adam: AdamConfig, step: int,
+               scale_mode: int = 0, scale=None, stream=None) -> None:
+    """a3 + a4 + a5 on the device (asynchronous)."""
+    sc = None
+    if scale is not None:
+        sc = np.ascontiguousarray(scale, dtype=np.float32)
+    a = L.MoeAdamT(adam.lr, adam.beta1, adam.beta2, adam.eps, adam.weight_decay, step, scale_mode,
+                   sc.ctypes.data_as(C.POINTER(C.c_float)) if sc is not None else None)
+    check(L.lib().moe_update(ctx.handle, C.byref(plan_cur.c), C.byref(plan_next.c), C.byref(a),
+                             _stream_ptr(stream)), "moe_update")
+
+
+def moe_place(ctx: MoeContext, plan: Plan, stream=None) -> None:
+    """a5 alone: bf16(master) into every slot of `plan` (initial placement)."""
+    check(L.lib().moe_place(ctx.handle, C.byref(plan.c), _stream_ptr(stream)), "moe_place")
+
+
+def synth_grads(dst: torch.Tensor, seed: int, t: int, slot_base: int, S: int, P: int,
+                stream=None) -> None:
+    check(L.lib().moe_synth_grads(_ptr(dst), seed, t, slot_base, S, P, _stream_ptr(stream)),
+          "moe_synth_grads")
+
+
+def synth_master(dst: torch.Tensor, seed: int, E: int, lo: int, n: int, stream=None) -> None:
+    check(L.lib().moe_synth_master(_ptr(dst), seed, E, lo, n, _stream_ptr(stream)),
+          "moe_synth_master")

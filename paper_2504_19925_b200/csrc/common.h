@@ -1,0 +1,27 @@
+// Error plumbing shared by every translation unit of libmoedc (host side only).
+#pragma once
+
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "moe_dc.h"
+
+namespace moe {
+
+inline std::string &last_error_buf() {
+  static thread_local std::string buf;
+  return buf;
+}
+
+inline int fail(int code, const char *fmt, ...) {
+  char tmp[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(tmp, sizeof(tmp), fmt, ap);
+  va_end(ap);
+  last_error_buf() = tmp;
+  return code;
+}
+
+}  // namespace moe

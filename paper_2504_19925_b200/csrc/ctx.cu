@@ -1,0 +1,260 @@
+// Context lifecycle: scratch, the cross-GPU sync buffer, CUDA-IPC peer mapping, error check.
+//
+// One process per GPU (real mode): every GPU's slot grads, slot weights and sync buffer are
+// mapped into every peer (CUDA IPC over NVLink/NVSwitch), so the fused kernels pull grads and
+// push weights with plain 16-byte loads/stores to peer HBM.  No NCCL and no
+// sub-communicators: the paper's N(N-1)/2 pre-registered groups are not
+// needed for one-sided transfers inside one box.
+//
+// Virtual mode (rank = -1): all G ranks' buffers live on one device and one launch covers all
+// of them -- the multi-rank index math and reduction order run on a single GPU.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+
+#include "internal.h"
+
+using namespace moe;
+
+int moe_update_blocks_per_sm();  // update.cu
+
+int moe_validate_plan(const moe_ctx *ctx, const moe_plan_t *p, const char *what) {
+  if (!p || !p->first_slot) return fail(MOE_ERR_INVALID, "%s: NULL plan", what);
+  if (p->E != ctx->E || p->G != ctx->G || p->S != ctx->S)
+    return fail(MOE_ERR_SHAPE, "%s: plan (E,G,S)=(%d,%d,%d) != context (%d,%d,%d)", what, p->E, p->G,
+                p->S, ctx->E, ctx->G, ctx->S);
+  if (p->first_slot[0] != 0 || p->first_slot[ctx->E] != ctx->G * ctx->S)
+    return fail(MOE_ERR_SHAPE, "%s: first_slot must run from 0 to G*S", what);
+  for (int e = 0; e < ctx->E; ++e)
+    if (p->first_slot[e + 1] - p->first_slot[e] < 1)
+      return fail(MOE_ERR_SHAPE, "%s: expert %d has no replica", what, e);
+  if (p->slot_expert)
+    for (int e = 0; e < ctx->E; ++e)
+      for (int j = p->first_slot[e]; j < p->first_slot[e + 1]; ++j)
+        if (p->slot_expert[j] != e)
+          return fail(MOE_ERR_SHAPE, "%s: slot_expert inconsistent with first_slot at slot %d", what, j);
+  return MOE_OK;
+}
+
+namespace {
+
+typedef int (*PFN_getAddressRange)(unsigned long long *, size_t *, unsigned long long);
+
+int alloc_base(const void *ptr, void **base) {
+  static PFN_getAddressRange fn = nullptr;
+  if (!fn) {
+    void *f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    MOE_CUDA_TRY(cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q));
+    if (!f || q != cudaDriverEntryPointSuccess)
+      return fail(MOE_ERR_COMM, "cuMemGetAddressRange entry point unavailable");
+    fn = (PFN_getAddressRange)f;
+  }
+  unsigned long long b = 0;
+  size_t sz = 0;
+  if (fn(&b, &sz, (unsigned long long)ptr) != 0)
+    return fail(MOE_ERR_COMM, "cuMemGetAddressRange failed for %p", ptr);
+  *base = (void *)b;
+  return MOE_OK;
+}
+
+void free_ctx(moe_ctx *c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  for (auto &kv : c->opened) cudaIpcCloseMemHandle(kv.second);
+  cudaFree(c->sync);
+  cudaFree(c->cnt_local);
+  cudaFree(c->done);
+  cudaFree(c->blk);
+  cudaFree(c->einfo);
+  cudaFree(c->counts_dev);
+  cudaFree(c->err);
+  if (c->counts_ev) cudaEventDestroy(c->counts_ev);
+  delete c;
+}
+
+}  // namespace
+
+extern "C" int moe_ctx_create(const moe_ctx_desc *d, moe_ctx **out) {
+  if (!d || !out) return fail(MOE_ERR_INVALID, "moe_ctx_create: NULL argument");
+  *out = nullptr;
+  if (d->E < 1 || d->G < 1 || d->S < 1 || d->k < 1)
+    return fail(MOE_ERR_INVALID, "moe_ctx_create: E, G, S, k must be >= 1");
+  if (d->E > MOE_MAX_E || d->G > MOE_MAX_G || (int64_t)d->G * d->S > MOE_MAX_SLOTS)
+    return fail(MOE_ERR_INVALID, "moe_ctx_create: limits E<=%d, G<=%d, G*S<=%d", MOE_MAX_E, MOE_MAX_G,
+                MOE_MAX_SLOTS);
+  if (d->E > d->G * d->S) return fail(MOE_ERR_INVALID, "moe_ctx_create: E > G*S");
+  if (d->k > d->E) return fail(MOE_ERR_INVALID, "moe_ctx_create: k > E");
+  if (d->P < 1 || d->P % d->G || (d->P / d->G) % kVec)
+    return fail(MOE_ERR_INVALID, "moe_ctx_create: need P %% G == 0 and (P/G) %% %d == 0 (pad)", kVec);
+  if (d->P >= (int64_t)1 << 40) return fail(MOE_ERR_INVALID, "moe_ctx_create: P too large");
+  if (d->max_tokens < 0 || (d->max_tokens * d->k) * d->G >= ((int64_t)1 << 31))
+    return fail(MOE_ERR_INVALID, "moe_ctx_create: max_tokens*k*G must fit int32");
+  if (d->rank < -1 || d->rank >= d->G) return fail(MOE_ERR_INVALID, "moe_ctx_create: rank out of range");
+  const int n_local = d->rank < 0 ? d->G : 1;
+  if (!d->slot_w || !d->slot_g || !d->master || !d->adam_m || !d->adam_v)
+    return fail(MOE_ERR_INVALID, "moe_ctx_create: NULL buffer table");
+  for (int v = 0; v < n_local; ++v) {
+    if (!d->slot_w[v] || !d->slot_g[v] || !d->master[v] || !d->adam_m[v] || !d->adam_v[v])
+      return fail(MOE_ERR_INVALID, "moe_ctx_create: NULL buffer for local rank %d", v);
+    const uintptr_t al = (uintptr_t)d->slot_w[v] | (uintptr_t)d->slot_g[v] | (uintptr_t)d->master[v] |
+                         (uintptr_t)d->adam_m[v] | (uintptr_t)d->adam_v[v];
+    if (al & 15) return fail(MOE_ERR_INVALID, "moe_ctx_create: buffers must be 16-byte aligned");
+  }
+  MOE_CUDA_TRY(cudaSetDevice(d->device));
+
+  moe_ctx *c = new moe_ctx();
+  c->E = d->E;
+  c->G = d->G;
+  c->S = d->S;
+  c->k = d->k;
+  c->P = d->P;
+  c->Pg = d->P / d->G;
+  c->max_tokens = d->max_tokens;
+  c->rank = d->rank;
+  c->n_local = n_local;
+  c->device = d->device;
+  c->connected = false;
+  c->disp_epoch = c->upd_epoch = 0;
+  c->sync = nullptr;
+  c->cnt_local = nullptr;
+  c->done = nullptr;
+  c->blk = nullptr;
+  c->einfo = nullptr;
+  c->counts_dev = nullptr;
+  c->err = nullptr;
+  c->counts_ev = nullptr;
+  c->counts_pending = false;
+  for (int v = 0; v < n_local; ++v) {
+    c->slot_w.push_back(d->slot_w[v]);
+    c->slot_g.push_back(d->slot_g[v]);
+    c->master.push_back(d->master[v]);
+    c->adam_m.push_back(d->adam_m[v]);
+    c->adam_v.push_back(d->adam_v[v]);
+  }
+  c->nb_max = std::max<int64_t>(1, (d->max_tokens * d->k + kTilePairs - 1) / kTilePairs);
+  cudaError_t e = cudaSuccess;
+  auto chk = [&](cudaError_t x) {
+    if (x != cudaSuccess && e == cudaSuccess) e = x;
+  };
+  chk(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, d->device));
+  chk(cudaMalloc(&c->sync, sizeof(SyncBuf)));
+  chk(cudaMalloc(&c->cnt_local, sizeof(int32_t) * n_local * c->E));
+  chk(cudaMalloc(&c->done, sizeof(uint32_t) * n_local));
+  chk(cudaMalloc(&c->blk, sizeof(int32_t) * n_local * c->E * c->nb_max));
+  chk(cudaMalloc(&c->einfo, sizeof(ExpertInfo) * n_local * c->E));
+  chk(cudaMalloc(&c->counts_dev, sizeof(int64_t) * c->E));
+  chk(cudaMalloc(&c->err, sizeof(int32_t)));
+  chk(cudaEventCreateWithFlags(&c->counts_ev, cudaEventDisableTiming));
+  if (e == cudaSuccess) {
+    chk(cudaMemset(c->sync, 0, sizeof(SyncBuf)));
+    chk(cudaMemset(c->cnt_local, 0, sizeof(int32_t) * n_local * c->E));
+    chk(cudaMemset(c->done, 0, sizeof(uint32_t) * n_local));
+    chk(cudaMemset(c->err, 0, sizeof(int32_t)));
+    chk(cudaDeviceSynchronize());
+  }
+  if (e != cudaSuccess) {
+    free_ctx(c);
+    return fail(MOE_ERR_CUDA, "moe_ctx_create: %s", cudaGetErrorString(e));
+  }
+  c->upd_blocks_per_sm = moe_update_blocks_per_sm();
+  for (int h = 0; h < MOE_MAX_G; ++h) {
+    c->peer_slot_g[h] = c->peer_slot_w[h] = nullptr;
+    c->peer_sync[h] = nullptr;
+  }
+  if (c->rank < 0) {  // virtual: every "peer" is local
+    for (int h = 0; h < c->G; ++h) {
+      c->peer_slot_g[h] = c->slot_g[h];
+      c->peer_slot_w[h] = c->slot_w[h];
+      c->peer_sync[h] = c->sync;
+    }
+    c->connected = true;
+  } else {
+    c->peer_slot_g[c->rank] = c->slot_g[0];
+    c->peer_slot_w[c->rank] = c->slot_w[0];
+    c->peer_sync[c->rank] = c->sync;
+    c->connected = (c->G == 1);
+  }
+  *out = c;
+  return MOE_OK;
+}
+
+extern "C" int moe_ctx_destroy(moe_ctx *ctx) {
+  free_ctx(ctx);
+  return MOE_OK;
+}
+
+extern "C" int moe_ctx_handle_bytes(void) { return (int)sizeof(IpcRecord); }
+
+extern "C" int moe_ctx_export(moe_ctx *ctx, void *out) {
+  if (!ctx || !out) return fail(MOE_ERR_INVALID, "moe_ctx_export: NULL argument");
+  if (ctx->rank < 0) return fail(MOE_ERR_INVALID, "moe_ctx_export: virtual-mode context");
+  MOE_CUDA_TRY(cudaSetDevice(ctx->device));
+  IpcRecord rec;
+  memset(&rec, 0, sizeof(rec));
+  const void *bufs[3] = {ctx->slot_g[0], ctx->slot_w[0], ctx->sync};
+  for (int i = 0; i < 3; ++i) {
+    void *base = nullptr;
+    int st = alloc_base(bufs[i], &base);
+    if (st) return st;
+    MOE_CUDA_TRY(cudaIpcGetMemHandle(&rec.h[i], base));
+    rec.off[i] = (uint64_t)((const char *)bufs[i] - (const char *)base);
+  }
+  memcpy(out, &rec, sizeof(rec));
+  return MOE_OK;
+}
+
+extern "C" int moe_ctx_connect(moe_ctx *ctx, const void *all) {
+  if (!ctx || !all) return fail(MOE_ERR_INVALID, "moe_ctx_connect: NULL argument");
+  if (ctx->rank < 0) return fail(MOE_ERR_INVALID, "moe_ctx_connect: virtual-mode context");
+  MOE_CUDA_TRY(cudaSetDevice(ctx->device));
+  const IpcRecord *recs = (const IpcRecord *)all;
+  for (int h = 0; h < ctx->G; ++h) {
+    if (h == ctx->rank) continue;
+    void *ptrs[3];
+    for (int i = 0; i < 3; ++i) {
+      std::string key((const char *)&recs[h].h[i], sizeof(cudaIpcMemHandle_t));
+      auto it = ctx->opened.find(key);
+      void *base = nullptr;
+      if (it != ctx->opened.end()) {
+        base = it->second;
+      } else {
+        cudaError_t e = cudaIpcOpenMemHandle(&base, recs[h].h[i], cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess)
+          return fail(MOE_ERR_COMM, "cudaIpcOpenMemHandle(peer %d, buffer %d): %s", h, i,
+                      cudaGetErrorString(e));
+        ctx->opened[key] = base;
+      }
+      ptrs[i] = (char *)base + recs[h].off[i];
+    }
+    ctx->peer_slot_g[h] = ptrs[0];
+    ctx->peer_slot_w[h] = ptrs[1];
+    ctx->peer_sync[h] = (SyncBuf *)ptrs[2];
+  }
+  ctx->connected = true;
+  return MOE_OK;
+}
+
+extern "C" int moe_ctx_wait_counts(moe_ctx *ctx) {
+  if (!ctx) return fail(MOE_ERR_INVALID, "moe_ctx_wait_counts: NULL ctx");
+  if (!ctx->counts_pending) return MOE_OK;
+  MOE_CUDA_TRY(cudaEventSynchronize(ctx->counts_ev));
+  return MOE_OK;
+}
+
+extern "C" int moe_ctx_check(moe_ctx *ctx, void *stream) {
+  if (!ctx) return fail(MOE_ERR_INVALID, "moe_ctx_check: NULL ctx");
+  MOE_CUDA_TRY(cudaSetDevice(ctx->device));
+  MOE_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+  int32_t err = 0;
+  MOE_CUDA_TRY(cudaMemcpy(&err, ctx->err, sizeof(err), cudaMemcpyDeviceToHost));
+  if (err) {
+    MOE_CUDA_TRY(cudaMemset(ctx->err, 0, sizeof(int32_t)));
+    MOE_CUDA_TRY(cudaDeviceSynchronize());
+    if (err & kErrTimeout) return fail(MOE_ERR_TIMEOUT, "a cross-GPU flag wait timed out");
+    return fail(MOE_ERR_DATA, "invalid topk ids (outside [0,E) or repeated within a token)");
+  }
+  return MOE_OK;
+}

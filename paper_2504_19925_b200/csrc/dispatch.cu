@@ -1,0 +1,380 @@
+// a0 count exchange + a2 replica-balanced dispatch.
+//
+// PAPER.md:687-689 (step 1): the router aggregates per-expert token counts across ranks;
+// PAPER.md:690-692 (step 2): "load-balances the tokens for a given expert class across its
+// replicated instances".  Reading A6: counts are (token, expert) pairs.  Reading A8: pairs
+// are ranked within their expert in global order (rank, token, choice); the first
+// m = C_e mod r_e replicas take q+1 = C_e div r_e + 1 pairs, the rest q, in contiguous chunks.
+//
+// Three launches per call, all integer work, bit-exact and deterministic (no atomics
+// decide any order):
+//   K1 k_hist    per-tile expert histograms (warp-aggregated shared-memory atomics); the
+//                last tile of each rank publishes the rank's [E] counts into every GPU's
+//                sync buffer with one-sided NVLink stores + a release flag (the paper's
+//                popularity all-reduce, done as an all-gather so it also yields the
+//                global rank bases).
+//   K2 k_scan    per expert: waits for all ranks' flags (acquire), C_e, this rank's base,
+//                q/m, slot loads, send counts; exclusive scan of the tile counts.
+//   K3 k_scatter per tile: stable within-tile rank via __match_any_sync + popc of lower
+//                lanes + a cross-warp prefix, then (slot, offset) and the slot-major
+//                send order.
+// Bytes (algorithmic, per pair): ids read twice (8), gates 4, dest_slot/dest_off/
+// send_pair/send_gate written 16 -> 28 B/pair.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "internal.h"
+
+namespace moe {
+namespace {
+
+struct HistArgs {
+  const int32_t *ids;
+  int64_t npairs;  // pairs per rank = T*k
+  int32_t k, E, G, rank, real, nb, nb_max;
+  uint32_t epoch;
+  int32_t parity;
+  int32_t *blk;        // [n_local][E][nb_max]
+  int32_t *cnt_local;  // [n_local][E]
+  uint32_t *done;      // [n_local]
+  int32_t *err;
+  SyncBuf *dst[MOE_MAX_G];  // real: every GPU's sync buffer; virtual: dst[0] = the shared one
+};
+
+__global__ void __launch_bounds__(kThreads) k_hist(const __grid_constant__ HistArgs a) {
+  __shared__ int32_t hist[MOE_MAX_E];
+  __shared__ int is_last;
+  const int v = blockIdx.x / a.nb;   // local rank
+  const int b = blockIdx.x % a.nb;   // tile
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int32_t *ids = a.ids + (int64_t)v * a.npairs;
+  for (int e = tid; e < a.E; e += kThreads) hist[e] = 0;
+  __syncthreads();
+
+  const int64_t t0 = (int64_t)b * kTilePairs;
+#pragma unroll 4
+  for (int i = 0; i < kTilePairs / kThreads; ++i) {
+    const int64_t p = t0 + i * kThreads + tid;
+    const bool in = p < a.npairs;
+    int e = in ? __ldg(ids + p) : -1;
+    bool valid = in && (unsigned)e < (unsigned)a.E;
+    if (in && !valid) atomicOr(a.err, kErrData);
+    if (valid && a.k > 1) {  // the k experts of a token must be distinct
+      const int j = (int)(p % a.k);
+      for (int jj = 0; jj < j; ++jj)
+        if (__ldg(ids + (p - j + jj)) == e) atomicOr(a.err, kErrData);
+    }
+    const unsigned act = __ballot_sync(0xffffffffu, valid);
+    if (valid) {
+      const unsigned peers = __match_any_sync(act, e);
+      if (lane == __ffs(peers) - 1) atomicAdd(&hist[e], __popc(peers));
+    }
+  }
+  __syncthreads();
+
+  int32_t *blk = a.blk + (int64_t)v * a.E * a.nb_max;
+  for (int e = tid; e < a.E; e += kThreads) {
+    const int32_t h = hist[e];
+    blk[(int64_t)e * a.nb_max + b] = h;
+    if (h) atomicAdd(a.cnt_local + v * a.E + e, h);
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) is_last = (atomicAdd(a.done + v, 1u) == (unsigned)(a.nb - 1));
+  __syncthreads();
+  if (!is_last) return;
+
+  // Last tile of rank v: publish the rank's counts (a0).
+  __threadfence();
+  const int grank = a.real ? a.rank : v;
+  for (int e = tid; e < a.E; e += kThreads) {
+    const int32_t c = atomicExch(a.cnt_local + v * a.E + e, 0);  // read + reset for next call
+    if (a.real) {
+      for (int h = 0; h < a.G; ++h) a.dst[h]->xcnt[a.parity][grank][e] = c;  // NVLink stores
+    } else {
+      a.dst[0]->xcnt[a.parity][grank][e] = c;
+    }
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (tid == 0) {
+    a.done[v] = 0;
+    if (a.real)
+      for (int h = 0; h < a.G; ++h) st_release_sys(&a.dst[h]->disp_flag[grank], a.epoch);
+  }
+}
+
+struct ScanArgs {
+  int32_t E, G, S, rank, real, nb, nb_max;
+  uint32_t epoch;
+  int32_t parity;
+  const SyncBuf *sync;  // this GPU's sync buffer
+  int32_t *blk;
+  ExpertInfo *einfo;     // [n_local][E]
+  int32_t *slot_load;    // [G*S]
+  int32_t *send_count;   // [n_local][G*S]
+  int64_t *counts_dev;   // [E]
+  int32_t *err;
+  int32_t fs[MOE_MAX_E + 1];
+};
+
+__device__ __forceinline__ int32_t ld_cg(const int32_t *p) { return __ldcg(p); }
+
+__global__ void __launch_bounds__(kThreads) k_scan(const __grid_constant__ ScanArgs a) {
+  const int e = blockIdx.x;
+  const int v = blockIdx.y;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int grank = a.real ? a.rank : v;
+  __shared__ int32_t s_base, s_cnt, s_C, s_loc;
+  __shared__ int32_t wsum[kThreads / 32];
+  __shared__ int ok;
+
+  if (tid == 0) {
+    ok = 1;
+    if (a.real)
+      for (int h = 0; h < a.G; ++h)
+        if (!wait_flag(&a.sync->disp_flag[h], a.epoch, a.err)) ok = 0;
+  }
+  __syncthreads();
+  if (!ok) return;
+  if (tid == 0) {
+    const int32_t(*x)[MOE_MAX_E] = a.sync->xcnt[a.parity];
+    int32_t C = 0, base = 0;
+    for (int h = 0; h < a.G; ++h) {
+      const int32_t c = ld_cg(&x[h][e]);
+      if (h < grank) base += c;
+      C += c;
+    }
+    int32_t loc = 0;
+    for (int e2 = 0; e2 < e; ++e2) loc += ld_cg(&x[grank][e2]);
+    s_base = base;
+    s_cnt = ld_cg(&x[grank][e]);
+    s_C = C;
+    s_loc = loc;
+  }
+  __syncthreads();
+  const int32_t C = s_C, base = s_base, cnt = s_cnt;
+  const int32_t f0 = a.fs[e], r = a.fs[e + 1] - f0;
+  const int32_t q = C / r, m = C % r;
+  const int GS = a.G * a.S;
+  if (v == 0) {
+    if (tid == 0) a.counts_dev[e] = C;
+    for (int rho = tid; rho < r; rho += kThreads) a.slot_load[f0 + rho] = q + (rho < m ? 1 : 0);
+  }
+  for (int rho = tid; rho < r; rho += kThreads) {
+    const int32_t start = rho * q + min(rho, m), len = q + (rho < m ? 1 : 0);
+    const int32_t lo = max(base, start), hi = min(base + cnt, start + len);
+    a.send_count[(int64_t)v * GS + f0 + rho] = max(0, hi - lo);
+  }
+  if (tid == 0) a.einfo[v * a.E + e] = ExpertInfo{base, s_loc, q, m};
+
+  // exclusive scan of this rank's tile counts of expert e, in place
+  int32_t *row = a.blk + ((int64_t)v * a.E + e) * a.nb_max;
+  const int per = (a.nb + kThreads - 1) / kThreads;
+  const int lo = tid * per, hi = min(a.nb, lo + per);
+  int32_t s = 0;
+  for (int i = lo; i < hi; ++i) s += row[i];
+  int32_t incl = s;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += y;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  int32_t woff = 0;
+  for (int w = 0; w < warp; ++w) woff += wsum[w];
+  int32_t run = woff + incl - s;
+  for (int i = lo; i < hi; ++i) {
+    const int32_t c = row[i];
+    row[i] = run;
+    run += c;
+  }
+}
+
+struct ScatterArgs {
+  const int32_t *ids;
+  const float *gates;
+  int64_t npairs;
+  int32_t E, nb, nb_max;
+  const int32_t *blk;
+  const ExpertInfo *einfo;
+  int32_t *dest_slot, *dest_off, *send_pair;
+  float *send_gate;
+  int32_t fs[MOE_MAX_E + 1];
+};
+
+__global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ ScatterArgs a) {
+  constexpr int kWarps = kThreads / 32;
+  constexpr int kRounds = kTilePairs / kThreads;  // 8 rounds of 32 consecutive pairs per warp
+  __shared__ int32_t wcnt[kWarps][MOE_MAX_E];
+  __shared__ ExpertInfo s_info[MOE_MAX_E];
+  __shared__ int32_t s_blk[MOE_MAX_E];
+  const int v = blockIdx.x / a.nb;
+  const int b = blockIdx.x % a.nb;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t off_v = (int64_t)v * a.npairs;
+  for (int e = tid; e < a.E; e += kThreads) {
+    s_info[e] = a.einfo[v * a.E + e];
+    s_blk[e] = a.blk[((int64_t)v * a.E + e) * a.nb_max + b];
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) wcnt[w][e] = 0;
+  }
+  __syncthreads();
+
+  // warp w owns the 256 consecutive pairs [w*256, (w+1)*256) of the tile, in 8 rounds of 32:
+  // pair order == (warp, round, lane) order, so ranks below are stable.
+  const int64_t seg = (int64_t)b * kTilePairs + warp * (kRounds * 32);
+  int32_t er[kRounds], rk[kRounds];
+  const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int r = 0; r < kRounds; ++r) {
+    const int64_t p = seg + r * 32 + lane;
+    const bool in = p < a.npairs;
+    const int e = in ? __ldg(a.ids + off_v + p) : -1;
+    const bool valid = in && (unsigned)e < (unsigned)a.E;
+    const unsigned act = __ballot_sync(0xffffffffu, valid);
+    unsigned peers = 0;
+    int myr = 0;
+    if (valid) {
+      peers = __match_any_sync(act, e);
+      myr = wcnt[warp][e] + __popc(peers & lt);
+    }
+    __syncwarp();
+    if (valid && lane == __ffs(peers) - 1) wcnt[warp][e] += __popc(peers);
+    __syncwarp();
+    er[r] = in ? (valid ? e : -2) : -1;
+    rk[r] = myr;
+  }
+  __syncthreads();
+  for (int e = tid; e < a.E; e += kThreads) {  // exclusive prefix over warps, per expert
+    int32_t run = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      const int32_t c = wcnt[w][e];
+      wcnt[w][e] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < kRounds; ++r) {
+    const int64_t p = seg + r * 32 + lane;
+    const int e = er[r];
+    if (e == -1) continue;
+    if (e < 0) {  // invalid id: flagged by k_hist; keep memory safe
+      a.dest_slot[off_v + p] = -1;
+      a.dest_off[off_v + p] = -1;
+      continue;
+    }
+    const ExpertInfo in = s_info[e];
+    const int32_t lr = s_blk[e] + wcnt[warp][e] + rk[r];  // rank within this rank's pairs of e
+    const int32_t R = in.base + lr;                         // global rank within expert e
+    const int32_t q = in.q, m = in.m;
+    const int32_t big = m * (q + 1);
+    const int32_t rho = R < big ? R / (q + 1) : m + (R - big) / q;
+    const int32_t off = R - (rho * q + min(rho, m));
+    a.dest_slot[off_v + p] = a.fs[e] + rho;
+    a.dest_off[off_v + p] = off;
+    const int64_t pos = off_v + in.loc_off + lr;
+    a.send_pair[pos] = (int32_t)p;
+    a.send_gate[pos] = __ldg(a.gates + off_v + p);
+  }
+}
+
+}  // namespace
+}  // namespace moe
+
+using namespace moe;
+
+int moe_validate_plan(const moe_ctx *ctx, const moe_plan_t *p, const char *what);  // ctx.cu
+
+extern "C" int moe_dispatch(moe_ctx *ctx, const int32_t *topk_ids, const float *gates, int64_t T,
+                            const moe_plan_t *plan, const moe_dispatch_out *out, void *stream) {
+  if (!ctx || !out) return fail(MOE_ERR_INVALID, "moe_dispatch: NULL ctx/out");
+  if (T < 0 || T > ctx->max_tokens)
+    return fail(MOE_ERR_INVALID, "moe_dispatch: T=%lld outside [0, max_tokens=%lld]", (long long)T,
+                (long long)ctx->max_tokens);
+  if ((T > 0 && (!topk_ids || !gates || !out->dest_slot || !out->dest_off || !out->send_pair ||
+                 !out->send_gate)) ||
+      !out->send_count || !out->slot_load)
+    return fail(MOE_ERR_INVALID, "moe_dispatch: NULL buffer");
+  if (ctx->rank >= 0 && ctx->G > 1 && !ctx->connected)
+    return fail(MOE_ERR_INVALID, "moe_dispatch: real-mode context not connected");
+  int st = moe_validate_plan(ctx, plan, "moe_dispatch");
+  if (st) return st;
+  MOE_CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t npairs = T * ctx->k;
+  const int nb = (int)std::max<int64_t>(1, (npairs + kTilePairs - 1) / kTilePairs);
+  const uint32_t epoch = ++ctx->disp_epoch;
+  const int parity = (int)(epoch & 1u);
+  const int real = ctx->rank >= 0 ? 1 : 0;
+
+  HistArgs ha{};
+  ha.ids = topk_ids;
+  ha.npairs = npairs;
+  ha.k = ctx->k;
+  ha.E = ctx->E;
+  ha.G = ctx->G;
+  ha.rank = ctx->rank;
+  ha.real = real;
+  ha.nb = nb;
+  ha.nb_max = (int)ctx->nb_max;
+  ha.epoch = epoch;
+  ha.parity = parity;
+  ha.blk = ctx->blk;
+  ha.cnt_local = ctx->cnt_local;
+  ha.done = ctx->done;
+  ha.err = ctx->err;
+  for (int h = 0; h < MOE_MAX_G; ++h) ha.dst[h] = real ? ctx->peer_sync[h] : ctx->sync;
+  k_hist<<<nb * ctx->n_local, kThreads, 0, s>>>(ha);
+  MOE_CUDA_TRY(cudaGetLastError());
+
+  ScanArgs sa{};
+  sa.E = ctx->E;
+  sa.G = ctx->G;
+  sa.S = ctx->S;
+  sa.rank = ctx->rank;
+  sa.real = real;
+  sa.nb = nb;
+  sa.nb_max = (int)ctx->nb_max;
+  sa.epoch = epoch;
+  sa.parity = parity;
+  sa.sync = ctx->sync;
+  sa.blk = ctx->blk;
+  sa.einfo = ctx->einfo;
+  sa.slot_load = out->slot_load;
+  sa.send_count = out->send_count;
+  sa.counts_dev = out->counts_dev ? out->counts_dev : ctx->counts_dev;
+  sa.err = ctx->err;
+  for (int e = 0; e <= ctx->E; ++e) sa.fs[e] = plan->first_slot[e];
+  k_scan<<<dim3(ctx->E, ctx->n_local), kThreads, 0, s>>>(sa);
+  MOE_CUDA_TRY(cudaGetLastError());
+  if (out->counts_host)  // C_t to the host planner while the scatter runs (PAPER.md:709 fn)
+    MOE_CUDA_TRY(cudaMemcpyAsync(out->counts_host, sa.counts_dev, sizeof(int64_t) * ctx->E,
+                                 cudaMemcpyDeviceToHost, s));
+  MOE_CUDA_TRY(cudaEventRecord(ctx->counts_ev, s));
+  ctx->counts_pending = true;
+
+  ScatterArgs ca{};
+  ca.ids = topk_ids;
+  ca.gates = gates;
+  ca.npairs = npairs;
+  ca.E = ctx->E;
+  ca.nb = nb;
+  ca.nb_max = (int)ctx->nb_max;
+  ca.blk = ctx->blk;
+  ca.einfo = ctx->einfo;
+  ca.dest_slot = out->dest_slot;
+  ca.dest_off = out->dest_off;
+  ca.send_pair = out->send_pair;
+  ca.send_gate = out->send_gate;
+  for (int e = 0; e <= ctx->E; ++e) ca.fs[e] = plan->first_slot[e];
+  if (npairs > 0) {
+    k_scatter<<<nb * ctx->n_local, kThreads, 0, s>>>(ca);
+    MOE_CUDA_TRY(cudaGetLastError());
+  }
+  return MOE_OK;
+}

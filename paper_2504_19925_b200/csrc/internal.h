@@ -1,0 +1,125 @@
+// Internal definitions of libmoedc: the context, the cross-GPU sync buffer, device helpers.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "common.h"
+
+namespace moe {
+
+constexpr int kThreads = 256;          // block size of every hot kernel
+constexpr int kTilePairs = 2048;       // dispatch tile: 8 warps x 8 rounds x 32 lanes
+constexpr int kVec = 8;                // elements per thread in the update (16 B of bf16)
+constexpr int kChunk = kThreads * kVec;  // update chunk: 2048 elements of one expert
+constexpr uint64_t kSpinTimeoutNs = 20ull * 1000 * 1000 * 1000;  // 20 s
+
+// Device-raised error bits (ctx->err)
+constexpr int kErrData = 1;
+constexpr int kErrTimeout = 2;
+
+// Cross-GPU sync buffer: one per GPU, mapped by every peer (CUDA IPC).  Peer g writes
+// its slot [g] of the flag arrays and its row of xcnt; the owner only reads them.
+struct SyncBuf {
+  alignas(128) uint32_t disp_flag[MOE_MAX_G];   // count exchange arrived (epoch)
+  alignas(128) uint32_t upd_in[MOE_MAX_G];      // update barrier-in (epoch)
+  alignas(128) uint32_t upd_out[MOE_MAX_G];     // update barrier-out (epoch)
+  alignas(128) int32_t xcnt[2][MOE_MAX_G][MOE_MAX_E];  // per-rank expert counts, by epoch parity
+};
+
+// Per-expert dispatch parameters computed by the scan kernel, read by the scatter kernel.
+struct ExpertInfo {
+  int32_t base;     // global rank of this rank's first pair of the expert
+  int32_t loc_off;  // offset of the expert's first pair in this rank's slot-major order
+  int32_t q, m;     // C_e / r_e, C_e % r_e
+};
+
+struct IpcRecord {
+  cudaIpcMemHandle_t h[3];  // slot_g, slot_w, sync
+  uint64_t off[3];          // byte offset of the buffer inside its allocation
+};
+
+}  // namespace moe
+
+struct moe_ctx {
+  int E, G, S, k;
+  int64_t P, Pg, max_tokens;
+  int rank;      // -1 virtual
+  int n_local;   // 1 (real) or G (virtual)
+  int device;
+  int num_sms;
+  int upd_blocks_per_sm;
+  bool connected;
+  uint32_t disp_epoch, upd_epoch;
+
+  // caller buffers, per local rank
+  std::vector<void *> slot_w, slot_g;
+  std::vector<float *> master, adam_m, adam_v;
+
+  // per-GPU views (index = GPU h in [0, G)); local or IPC-mapped peer pointers
+  void *peer_slot_g[MOE_MAX_G];
+  void *peer_slot_w[MOE_MAX_G];
+  moe::SyncBuf *peer_sync[MOE_MAX_G];
+
+  // library-owned device scratch
+  moe::SyncBuf *sync;       // this GPU's sync buffer (virtual mode: the single shared one)
+  int32_t *cnt_local;       // [n_local][E]
+  uint32_t *done;           // [n_local] last-block tickets of the histogram kernel
+  int32_t *blk;             // [n_local][E][nb_max] block counts, scanned in place
+  moe::ExpertInfo *einfo;   // [n_local][E]
+  int64_t *counts_dev;      // [E]
+  int32_t *err;             // device error bits
+  int64_t nb_max;
+  cudaEvent_t counts_ev;    // recorded after the C_e device->host copy
+  bool counts_pending;
+
+  std::map<std::string, void *> opened;  // IPC handle bytes -> mapped base (dedup)
+};
+
+namespace moe {
+
+// ------------------------------- device helpers -------------------------------------------
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void st_release_sys(uint32_t *p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Waits until *p reaches `epoch` (wrap-safe).  Returns false on timeout (and raises the
+// timeout error bit) so a missing peer never hangs the GPU.
+__device__ __forceinline__ bool wait_flag(const uint32_t *p, uint32_t epoch, int32_t *err) {
+  const uint64_t t0 = globaltimer();
+  while ((int32_t)(ld_acquire_sys(p) - epoch) < 0) {
+    if (globaltimer() - t0 > kSpinTimeoutNs) {
+      atomicOr(err, kErrTimeout);
+      return false;
+    }
+    __nanosleep(64);
+  }
+  return true;
+}
+
+}  // namespace moe
+
+#define MOE_CUDA_TRY(expr)                                                                   \
+  do {                                                                                      \
+    cudaError_t _e = (expr);                                                                \
+    if (_e != cudaSuccess)                                                                  \
+      return moe::fail(MOE_ERR_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__, \
+                       __LINE__);                                                           \
+  } while (0)

@@ -1,0 +1,92 @@
+"""DecoupledExpertLayer: the user-facing object for one MoE layer's decoupled expert state.
+
+It allocates (through PyTorch) the buffers the C ABI binds -- slot weights/grads [S][P] bf16
+and the owner's fp32 master/m/v shard [E][P/G] -- creates the context, and drives one
+iteration of the hot path in the paper's order (fig:design_diagram):
+
+    moe_dispatch(plan_t)      a0 count exchange + a2 replica-balanced dispatch   (device)
+    wait for C_t              (only the small D2H copy; the scatter keeps running)
+    moe_plan(C_t)             a1 Alg. 1 -> plan_{t+1}                              (host C++)
+    moe_update(plan_t, plan_{t+1})   a3 reduce + a4 Adam + a5 place               (device)
+
+Argument marshalling and ordering only; every stage runs in libmoedc.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import api
+
+
+class DecoupledExpertLayer:
+    def __init__(self, E: int, G: int, S: int, k: int, P: int, max_tokens: int, rank: int = -1,
+                 device: int | None = None, seed: int = 0, adam: api.AdamConfig | None = None,
+                 policy: int = api.MOE_PLAN_PAPER_ALG1, scale_mode: int = 0, scale=None,
+                 init_master: bool = True):
+        if device is None:
+            device = torch.cuda.current_device()
+        self.E, self.G, self.S, self.k, self.P = E, G, S, k, P
+        self.Pg = P // G
+        self.rank = rank
+        self.n_local = G if rank < 0 else 1
+        self.max_tokens = max_tokens
+        self.device = device
+        self.adam = adam or api.AdamConfig()
+        self.policy, self.scale_mode, self.scale = policy, scale_mode, scale
+        dev = torch.device("cuda", device)
+        n = self.n_local
+        self.slot_w = [torch.empty(S * P, dtype=torch.bfloat16, device=dev) for _ in range(n)]
+        self.slot_g = [torch.zeros(S * P, dtype=torch.bfloat16, device=dev) for _ in range(n)]
+        self.master = [torch.empty(E * self.Pg, dtype=torch.float32, device=dev) for _ in range(n)]
+        self.adam_m = [torch.zeros(E * self.Pg, dtype=torch.float32, device=dev) for _ in range(n)]
+        self.adam_v = [torch.zeros(E * self.Pg, dtype=torch.float32, device=dev) for _ in range(n)]
+        self.ctx = api.MoeContext(E, G, S, k, P, max_tokens, rank, self.slot_w, self.slot_g,
+                                  self.master, self.adam_m, self.adam_v, device=device)
+        self.out = api.DispatchBuffers(self.ctx, max_tokens)
+        self.seed = seed
+        if init_master:
+            for v in range(n):
+                owner = v if rank < 0 else rank
+                api.synth_master(self.master[v], seed, E, owner * self.Pg, self.Pg)
+        # plan_0 = Alg1(ones(E)) (reading A3)
+        self.plan = api.moe_plan(np.zeros(E, dtype=np.int64), E, G, S, policy)
+        self.t = 1  # Adam step (shared by all experts)
+        self._connected = (rank < 0 or G == 1)
+        if self._connected and init_master:
+            api.moe_place(self.ctx, self.plan)
+
+    # ---- multi-GPU -------------------------------------------------------------------------
+    def connect(self, group=None) -> None:
+        """Real mode: exchange CUDA-IPC records over torch.distributed, map peers, place plan_0."""
+        if self.rank >= 0 and self.G > 1:
+            self.ctx.connect_process_group(group)
+            self._connected = True
+            api.moe_place(self.ctx, self.plan)
+
+    # ---- one iteration ---------------------------------------------------------------------
+    def dispatch(self, topk_ids: torch.Tensor, gates: torch.Tensor, T: int, stream=None):
+        api.moe_dispatch(self.ctx, topk_ids, gates, T, self.plan, self.out, stream)
+        return self.out
+
+    def plan_next(self) -> api.Plan:
+        self.ctx.wait_counts()
+        return api.moe_plan(self.out.counts_host.numpy(), self.E, self.G, self.S, self.policy)
+
+    def update(self, plan_next: api.Plan, stream=None) -> None:
+        api.moe_update(self.ctx, self.plan, plan_next, self.adam, self.t, self.scale_mode,
+                       self.scale, stream)
+        self.plan = plan_next
+        self.t += 1
+
+    def iterate(self, topk_ids: torch.Tensor, gates: torch.Tensor, T: int, stream=None) -> api.Plan:
+        """The whole per-iteration hot path: dispatch -> plan -> reduce/Adam/place."""
+        if not self._connected:
+            raise RuntimeError("real-mode layer: call connect() first")
+        self.dispatch(topk_ids, gates, T, stream)
+        nxt = self.plan_next()
+        self.update(nxt, stream)
+        return nxt
+
+    def close(self) -> None:
+        self.ctx.close()

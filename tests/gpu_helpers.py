@@ -1,0 +1,100 @@
+"""Shared driver for GPU parity tests: runs the CUDA path (through the C ABI) and the CPU
+oracle on the same seeded inputs and compares every output of every iteration."""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from oracle import step as ostep
+from synth import configs, hashgen, traces
+
+
+def _u32(x: np.ndarray) -> np.ndarray:
+    return np.ascontiguousarray(x).view(np.uint32)
+
+
+def run_parity(name: str, G: int, iters: int, *, rank_mode: str = "virtual", idx=None,
+               T: int | None = None, policy: int = 0, scale_mode: int = 0, scale=None,
+               weight_decay: float = 0.0, trace=None, check_dispatch: bool = True):
+    """Returns the number of iterations compared.  rank_mode: "virtual" (rank=-1, G ranks on
+    cuda:0) or "single" (real mode with G == 1)."""
+    from paper_2504_19925_b200 import AdamConfig, DecoupledExpertLayer
+    from paper_2504_19925_b200.api import synth_grads
+    from oracle.adam import AdamHyper
+
+    wl = configs.CONFIGS[name]
+    S = wl.S(G)
+    E, k, P = wl.E, wl.k, wl.P
+    TT = wl.T if T is None else T
+    Tg = TT // G
+    seed = configs.seed_for(name)
+    rank = -1 if rank_mode == "virtual" else 0
+    if rank == 0:
+        assert G == 1
+    hyper = AdamHyper(weight_decay=weight_decay)
+    adam = AdamConfig(lr=hyper.lr, beta1=hyper.beta1, beta2=hyper.beta2, eps=hyper.eps,
+                      weight_decay=weight_decay)
+    layer = DecoupledExpertLayer(E, G, S, k, P, Tg, rank=rank, device=0, seed=seed, adam=adam,
+                                 policy=policy, scale_mode=scale_mode, scale=scale)
+    pol = "alg1" if policy == 0 else "minmax"
+    idx_arr = np.arange(P, dtype=np.int64) if idx is None else np.asarray(idx, dtype=np.int64)
+    sim = ostep.OracleSim(E, G, S, P, seed, hyper=hyper, policy=pol, scale_mode=scale_mode,
+                          scale=scale, idx=idx_arr)
+    idx_t = torch.from_numpy(idx_arr).cuda()
+    Pg = P // G
+    # initial placement (moe_place) equals the oracle's plan_0 placement
+    _compare_weights(layer, sim, idx_t, G, S, P)
+    tr = trace if trace is not None else traces.make_trace(wl, iters=iters, T=TT)
+    for t, (ids, gates) in enumerate(tr[:iters]):
+        for v in range(layer.n_local):
+            synth_grads(layer.slot_g[v], seed, t, v * S, S, P)
+        ids_d = torch.from_numpy(np.ascontiguousarray(ids)).cuda()
+        gates_d = torch.from_numpy(np.ascontiguousarray(gates)).cuda()
+        layer.iterate(ids_d, gates_d, Tg)
+        res = sim.iterate(traces.split_ranks(ids, G), traces.split_ranks(gates, G),
+                          lambda j, t=t: hashgen.grad_bits(seed, t, j, idx_arr.astype(np.uint64)))
+        layer.ctx.check()
+        pn = res["plan_next"]
+        assert layer.plan.replicas.tolist() == pn["replicas"].tolist(), f"iter {t}: replicas"
+        assert layer.plan.first_slot.tolist() == pn["first_slot"].tolist()
+        assert layer.plan.slot_expert.tolist() == pn["slot_expert"].tolist()
+        d = res["dispatch"]
+        assert layer.out.counts_host.tolist() == d["C"].tolist(), f"iter {t}: counts"
+        assert layer.out.slot_load.cpu().tolist() == d["slot_load"].tolist(), f"iter {t}: slot_load"
+        if check_dispatch:
+            n = Tg * k
+            ds = layer.out.dest_slot.cpu().numpy()
+            do = layer.out.dest_off.cpu().numpy()
+            sp = layer.out.send_pair.cpu().numpy()
+            sg = layer.out.send_gate.cpu().numpy()
+            sc = layer.out.send_count.cpu().numpy()
+            for v in range(G):
+                rk = d["ranks"][v]
+                sl = slice(v * n, (v + 1) * n)
+                assert np.array_equal(ds[sl], rk["dest_slot"]), f"iter {t} rank {v}: dest_slot"
+                assert np.array_equal(do[sl], rk["dest_off"]), f"iter {t} rank {v}: dest_off"
+                assert np.array_equal(sp[sl], rk["send_pair"]), f"iter {t} rank {v}: send_pair"
+                assert np.array_equal(_u32(sg[sl]), _u32(rk["send_gate"])), f"iter {t}: send_gate"
+                GS = G * S
+                assert np.array_equal(sc[v * GS:(v + 1) * GS], rk["send_count"]), f"iter {t}: send_count"
+        # optimizer state, bitwise (north_star: within 1e-6; the O6 op order makes it bitwise)
+        for v in range(G):
+            sel = (idx_t >= v * Pg) & (idx_t < (v + 1) * Pg)
+            if not bool(sel.any()):
+                continue
+            li = (idx_t[sel] - v * Pg)
+            cols = sel.cpu().numpy()
+            for name_, arr, want in (("master", layer.master, sim.master), ("m", layer.adam_m, sim.m),
+                                     ("v", layer.adam_v, sim.v)):
+                got = arr[v].view(E, Pg)[:, li].cpu().numpy()
+                assert np.array_equal(_u32(got), _u32(want[:, cols])), f"iter {t} owner {v}: {name_}"
+        _compare_weights(layer, sim, idx_t, G, S, P, t)
+    layer.close()
+    return iters
+
+
+def _compare_weights(layer, sim, idx_t, G, S, P, t=-1):
+    for v in range(G):
+        w = layer.slot_w[v].view(torch.int16).view(S, P)[:, idx_t].cpu().numpy().view(np.uint16)
+        want = sim.w_slot[v * S:(v + 1) * S]
+        assert np.array_equal(w, want), f"iter {t} GPU {v}: slot weights (bf16) differ"

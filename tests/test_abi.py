@@ -1,0 +1,108 @@
+"""C-ABI checks that need no GPU: the library loads, exports every symbol include/*.h
+declares, and its host-only planner (moe_plan) is bit-exact against the oracle.
+"""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import plan as OP
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_2504_19925_b200 import _lib
+    return _lib.lib()
+
+
+def _declared():
+    names = set()
+    for h in ("moe_dc.h", "moe_synth.h"):
+        src = open(os.path.join(ROOT, "include", h)).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        names |= set(re.findall(r"\b(moe_[a-z_0-9]+)\s*\(", src))
+    return names
+
+
+def test_exports_every_declared_symbol(lib):
+    from paper_2504_19925_b200 import _lib
+    declared = _declared()
+    assert declared, "no declarations parsed"
+    assert declared == set(_lib.EXPORTED)
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert lib.moe_abi_version() == 1
+    assert lib.moe_status_str(3) == b"MOE_ERR_DATA"
+    assert lib.moe_ctx_handle_bytes() >= 3 * 64
+
+
+def test_moe_plan_matches_oracle_fuzz(lib):
+    from paper_2504_19925_b200 import api
+    rng = np.random.default_rng(123)
+    for it in range(10_000):
+        E = int(rng.integers(1, 65))
+        G = int(rng.integers(1, 9))
+        s_min = -(-E // G)
+        S = int(rng.integers(s_min, max(s_min, 256 // G) + 1))
+        kind = it % 4
+        if kind == 0:
+            c = rng.integers(0, 1000, size=E)
+        elif kind == 1:
+            c = np.zeros(E, dtype=np.int64)
+            c[rng.integers(0, E)] = int(rng.integers(1, 10**9))
+        elif kind == 2:
+            c = (rng.pareto(1.1, size=E) * 1000).astype(np.int64)
+        else:
+            c = np.zeros(E, dtype=np.int64)
+        p, steps = api.moe_plan(c, E, G, S, return_steps=True)
+        r, osteps = OP.alg1(c, E, G, S, return_steps=True)
+        assert p.replicas.tolist() == r.tolist()
+        assert steps == osteps                           # identical correction sequence length
+        fs, se = OP.placement(r)
+        assert p.first_slot.tolist() == fs.tolist() and p.slot_expert.tolist() == se.tolist()
+        if it % 10 == 0:
+            pm = api.moe_plan(c, E, G, S, policy=api.MOE_PLAN_MINMAX)
+            assert pm.replicas.tolist() == OP.minmax(c, E, G, S).tolist()
+
+
+def test_moe_plan_extreme_skew_heap(lib):
+    from paper_2504_19925_b200 import api
+    for E, G, S in [(128, 8, 32), (256, 8, 64), (64, 1, 128)]:
+        c = np.ones(E, dtype=np.int64)
+        c[E // 3] = 10**12
+        p, steps = api.moe_plan(c, E, G, S, return_steps=True)
+        r, osteps = OP.alg1(c, E, G, S, return_steps=True)
+        assert p.replicas.tolist() == r.tolist() and steps == osteps
+        assert steps[0] > 2 * G * S
+
+
+def test_moe_plan_errors(lib):
+    from paper_2504_19925_b200 import api
+    with pytest.raises(api.MoeError) as ei:
+        api.moe_plan(np.ones(5, np.int64), 5, 1, 4)
+    assert ei.value.status == 1 and b"E=5 > G*S=4" in lib.moe_last_error()
+    with pytest.raises(api.MoeError):
+        api.moe_plan(np.array([1, -1], np.int64), 2, 1, 4)
+    with pytest.raises(api.MoeError):
+        api.moe_plan(np.ones(300, np.int64), 300, 8, 64)      # E > MOE_MAX_E
+    with pytest.raises(api.MoeError):
+        api.moe_plan(np.ones(4, np.int64), 4, 9, 4)           # G > MOE_MAX_G
+    plan = api.Plan(2, 1, 4)
+    st = lib.moe_plan_ex(np.ones(2, np.int64).ctypes.data_as(C.POINTER(C.c_int64)), 2, 1, 4, 7,
+                         C.byref(plan.c), None)
+    assert st == 1
+
+
+def test_spec_examples_through_abi(lib, golden_dir):
+    import json
+    from paper_2504_19925_b200 import api
+    g = json.load(open(os.path.join(golden_dir, "plan_examples.json")))
+    for ex in g["compute_placement"]:
+        p = api.moe_plan(np.array(ex["popularity"]), len(ex["popularity"]), 1, ex["slots_total"])
+        assert p.replicas.tolist() == ex["replicas"], ex["cite"]

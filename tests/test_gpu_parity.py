@@ -1,0 +1,149 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle, element by element.
+
+Bars (north_star): plan and dispatch indices bit-exact; master/m/v within 1e-6 relative --
+asserted BITWISE here, which the fixed op order makes achievable; bf16 weights exactly the
+RNE of the oracle's fp32 master, in every slot of the next placement.
+"""
+import numpy as np
+import pytest
+import torch
+
+from synth import configs, hashgen, traces
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    import __graft_entry__
+    __graft_entry__.build()
+    torch.cuda.set_device(0)
+
+
+def test_cuda_extension_is_the_path():
+    from paper_2504_19925_b200 import _lib
+    import os
+    L = _lib.lib()
+    assert os.path.samefile(L._name, _lib.LIB_PATH)
+    maps = open("/proc/self/maps").read()
+    assert "libmoedc.so" in maps
+
+
+@pytest.mark.parametrize("name", ["tiny", "tiny-skew", "tiny-odd"])
+def test_tiny_configs_20_iterations_virtual(name):
+    """All five rows, every iteration, G simulated GPUs in one device (virtual mode)."""
+    from gpu_helpers import run_parity
+    wl = configs.CONFIGS[name]
+    run_parity(name, wl.G_default, 20)
+
+
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+def test_tiny_skew_any_G(G):
+    """Same workload at every G with S*G fixed: the global dispatch is G-invariant and
+    the two-level reduce order follows the GPU boundaries."""
+    from gpu_helpers import run_parity
+    run_parity("tiny-skew", G, 6)
+
+
+def test_single_gpu_real_mode():
+    from gpu_helpers import run_parity
+    run_parity("tiny-skew", 1, 5, rank_mode="single")
+
+
+def test_minmax_policy_and_weight_decay_and_scale_modes():
+    from gpu_helpers import run_parity
+    run_parity("tiny-odd", 3, 4, policy=1, weight_decay=0.01)
+    run_parity("tiny-skew", 4, 3, scale_mode=1)
+    sc = np.linspace(0.25, 2.0, 8).astype(np.float32)
+    run_parity("tiny-skew", 4, 3, scale_mode=2, scale=sc)
+
+
+def test_rotating_hot_trace_tiny():
+    from gpu_helpers import run_parity
+    wl = configs.CONFIGS["tiny-skew"]
+    tr = traces.rotating_hot(wl.E, wl.T, wl.k, 7, seed=3)
+    run_parity("tiny-skew", 4, 7, trace=tr)
+
+
+def test_edge_cases_empty_and_degenerate():
+    from gpu_helpers import run_parity
+    E, k = 8, 2
+    # empty iteration (T = 0 on every rank), then an all-to-one-expert iteration, then k = E
+    tr = [(np.zeros((0, k), np.int32), np.zeros((0, k), np.float32))]
+    ids = np.stack([np.array([3, 5], np.int32)] * 4096)
+    tr.append((ids, np.full((4096, k), 0.5, np.float32)))
+    rng = np.random.default_rng(0)
+    ids = np.stack([rng.permutation(E)[:k] for _ in range(4096)]).astype(np.int32)
+    tr.append((ids, rng.random((4096, k)).astype(np.float32)))
+    # mix of T per iteration is not allowed by the layer (fixed T); run them separately
+    for i, (ids, gates) in enumerate(tr):
+        run_parity("tiny-skew", 4, 1, trace=[(ids, gates)], T=ids.shape[0])
+
+
+def test_invalid_ids_raise_data_error():
+    from paper_2504_19925_b200 import DecoupledExpertLayer, MoeError
+    layer = DecoupledExpertLayer(8, 1, 8, 2, 4096, 128, rank=0, device=0)
+    ids = torch.zeros((128, 2), dtype=torch.int32, device="cuda")
+    ids[:, 1] = 1
+    ids[7, 1] = 8                        # outside [0, E)
+    gates = torch.ones((128, 2), dtype=torch.float32, device="cuda")
+    layer.dispatch(ids, gates, 128)
+    with pytest.raises(MoeError) as ei:
+        layer.ctx.check()
+    assert ei.value.status == 3
+    ids[7, 1] = 0                        # repeated within a token
+    layer.dispatch(ids, gates, 128)
+    with pytest.raises(MoeError) as ei:
+        layer.ctx.check()
+    assert ei.value.status == 3
+    ids[7, 1] = 1
+    layer.dispatch(ids, gates, 128)
+    layer.ctx.check()                    # clean again
+    layer.close()
+
+
+def test_plan_shape_mismatch_rejected():
+    from paper_2504_19925_b200 import DecoupledExpertLayer, MoeError, api
+    layer = DecoupledExpertLayer(8, 1, 8, 2, 4096, 128, rank=0, device=0)
+    bad = api.moe_plan(np.ones(8, np.int64), 8, 1, 16)
+    with pytest.raises(MoeError) as ei:
+        api.moe_update(layer.ctx, bad, bad, layer.adam, 1)
+    assert ei.value.status == 2
+    layer.close()
+
+
+def test_synth_kernels_match_numpy_generator():
+    from paper_2504_19925_b200.api import synth_grads, synth_master
+    S, P = 3, 100_000
+    g = torch.empty(S * P, dtype=torch.bfloat16, device="cuda")
+    synth_grads(g, 77, 5, 9, S, P)
+    want = hashgen.grads_for_slots(77, 5, range(9, 12), P)
+    assert np.array_equal(g.view(torch.int16).cpu().numpy().view(np.uint16).reshape(S, P), want)
+    m = torch.empty(4 * 5000, dtype=torch.float32, device="cuda")
+    synth_master(m, 77, 4, 12345, 5000)
+    idx = np.arange(12345, 17345, dtype=np.uint64)
+    want = np.stack([hashgen.master_bits(77, e, idx) for e in range(4)])
+    assert np.array_equal(m.view(torch.int32).cpu().numpy().view(np.uint32).reshape(4, 5000), want)
+
+
+def _sample_idx(P: int, G: int, n: int = 2048) -> np.ndarray:
+    """Random elements plus every owner's first/last elements and chunk boundaries."""
+    rng = np.random.default_rng(P % 1000)
+    Pg = P // G
+    pts = set(rng.integers(0, P, n).tolist())
+    for g in range(G):
+        for off in (0, 1, 7, 8, 2047, 2048, Pg - 8, Pg - 1):
+            if 0 <= off < Pg:
+                pts.add(g * Pg + off)
+    return np.array(sorted(pts), dtype=np.int64)
+
+
+@pytest.mark.parametrize("name,G,iters", [("gpt-small", 1, 3), ("stress", 1, 3),
+                                          ("gpt-small", 8, 2), ("qwen3-fine", 1, 2)])
+def test_full_size_sampled(name, G, iters):
+    """BASELINE.json full sizes in the launch configuration bench.py times: the whole
+    dispatch is compared exactly; reduce/Adam/place on sampled elements of every expert and
+    every slot (the oracle computes them one by one)."""
+    from gpu_helpers import run_parity
+    wl = configs.CONFIGS[name]
+    run_parity(name, G, iters, idx=_sample_idx(wl.P, G))
