@@ -66,6 +66,16 @@ def moe_plan(counts, E: int, G: int, slots: int, policy: int = MOE_PLAN_PAPER_AL
     return (p, (int(steps[0]), int(steps[1]))) if return_steps else p
 
 
+def gather_records(record: bytes, G: int, group=None) -> list[bytes]:
+    """All-gather one opaque peer-mapping record per rank, in rank order (process-group plumbing)."""
+    import torch.distributed as dist
+    if dist.get_world_size(group) != G:
+        raise ValueError("process group size != G")
+    recs = [None] * G
+    dist.all_gather_object(recs, record, group=group)
+    return [bytes(r) for r in recs]
+
+
 class MoeContext:
     """moe_ctx: binds slot weights/grads and the owner's optimizer shards (caller tensors).
 
@@ -125,10 +135,7 @@ class MoeContext:
 
     def connect_process_group(self, group=None) -> None:
         """Exchange the CUDA-IPC records over a torch.distributed group and map the peers."""
-        import torch.distributed as dist
-        recs = [None] * self.G
-        dist.all_gather_object(recs, self.export(), group=group)
-        self.connect(recs)
+        self.connect(gather_records(self.export(), self.G, group))
 
     def wait_counts(self) -> None:
         """Host waits for the C_e copy of the last moe_dispatch (not for its scatter)."""

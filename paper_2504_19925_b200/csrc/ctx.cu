@@ -18,7 +18,7 @@
 
 using namespace moe;
 
-int moe_update_blocks_per_sm();  // update.cu
+int moe_update_init();  // update.cu
 
 int moe_validate_plan(const moe_ctx *ctx, const moe_plan_t *p, const char *what) {
   if (!p || !p->first_slot) return fail(MOE_ERR_INVALID, "%s: NULL plan", what);
@@ -159,7 +159,15 @@ extern "C" int moe_ctx_create(const moe_ctx_desc *d, moe_ctx **out) {
     free_ctx(c);
     return fail(MOE_ERR_CUDA, "moe_ctx_create: %s", cudaGetErrorString(e));
   }
-  c->upd_blocks_per_sm = moe_update_blocks_per_sm();
+  c->upd_blocks_per_sm = moe_update_init();
+  if (c->upd_blocks_per_sm < 0) {
+    free_ctx(c);
+    return fail(MOE_ERR_CUDA, "moe_ctx_create: update kernel setup failed");
+  }
+  {  // A/B switch for the update kernel: MOE_UPDATE_KERNEL=ldg selects the register-staged one
+    const char *k = getenv("MOE_UPDATE_KERNEL");
+    c->update_kernel = (k && std::string(k) == "ldg") ? 0 : 1;
+  }
   for (int h = 0; h < MOE_MAX_G; ++h) {
     c->peer_slot_g[h] = c->peer_slot_w[h] = nullptr;
     c->peer_sync[h] = nullptr;

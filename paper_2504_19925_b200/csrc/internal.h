@@ -54,6 +54,7 @@ struct moe_ctx {
   int device;
   int num_sms;
   int upd_blocks_per_sm;
+  int update_kernel;  // 1: k_update_tma (bulk-copy rings, default); 0: k_update (register-staged)
   bool connected;
   uint32_t disp_epoch, upd_epoch;
 

@@ -37,6 +37,8 @@ struct UpdArgs {
   int32_t fs_cur[MOE_MAX_E + 1];
   int32_t fs_next[MOE_MAX_E + 1];
   float scale[MOE_MAX_E];
+  uint8_t h_first_cur[MOE_MAX_E];   // GPU of expert e's first slot under plan_cur  (fs / S)
+  uint8_t h_first_next[MOE_MAX_E];  // ... under plan_next
   const uint16_t *gbase[MOE_MAX_G];  // bf16 [S][P] slot grads, per GPU
   uint16_t *wbase[MOE_MAX_G];        // bf16 [S][P] slot weights, per GPU
   float *master[MOE_MAX_G];          // fp32 [E][Pg], per owner
@@ -71,6 +73,39 @@ __device__ __forceinline__ uint32_t bf16_rne_bits(float x) {
   return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(x));
 }
 
+constexpr int kBatch = 8;  // replica grad slices loaded per round (16 B each, in flight together)
+
+// a5: the 16-byte bf16 vector -> every slot j of plan_next hosting e; slot j is on GPU j / S.
+__device__ __forceinline__ void place_to(const UpdArgs &a, int e, int64_t gi, const uint4 &wb) {
+  const int n0 = a.fs_next[e], n1 = a.fs_next[e + 1];
+  int h = a.h_first_next[e], l = n0 - h * a.S;
+  for (int j = n0; j < n1; ++j) {
+    st_stream(a.wbase[h] + (int64_t)l * a.P + gi, wb);
+    if (++l == a.S) {
+      l = 0;
+      ++h;
+    }
+  }
+}
+
+// a4: Adam on 8 elements, reading A15 op order, IEEE fp32 RN per op, bf16 RNE out.
+__device__ __forceinline__ void adam8(const UpdArgs &a, const float (&tot)[8], float sc, float (&w)[8],
+                                      float (&m)[8], float (&v)[8], uint4 &wb) {
+  uint32_t ob[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float g = __fmul_rn(tot[i], sc);
+    m[i] = __fadd_rn(__fmul_rn(a.b1, m[i]), __fmul_rn(a.omb1, g));
+    v[i] = __fadd_rn(__fmul_rn(a.b2, v[i]), __fmul_rn(a.omb2, __fmul_rn(g, g)));
+    const float den = __fadd_rn(__fdiv_rn(__fsqrt_rn(v[i]), a.rbc2), a.eps);
+    if (a.wd_on) w[i] = __fsub_rn(w[i], __fmul_rn(a.lrwd, w[i]));
+    w[i] = __fsub_rn(w[i], __fmul_rn(a.step, __fdiv_rn(m[i], den)));
+    ob[i] = bf16_rne_bits(w[i]);
+  }
+  wb = make_uint4(ob[0] | (ob[1] << 16), ob[2] | (ob[3] << 16), ob[4] | (ob[5] << 16),
+                  ob[6] | (ob[7] << 16));
+}
+
 __global__ void __launch_bounds__(kThreads) k_update(const __grid_constant__ UpdArgs a) {
   const int64_t per_owner = (int64_t)a.E * a.nchunks;
   const int64_t total = per_owner * a.o_count;
@@ -90,10 +125,7 @@ __global__ void __launch_bounds__(kThreads) k_update(const __grid_constant__ Upd
                                   bf16_rne_bits(x0.z) | (bf16_rne_bits(x0.w) << 16),
                                   bf16_rne_bits(x1.x) | (bf16_rne_bits(x1.y) << 16),
                                   bf16_rne_bits(x1.z) | (bf16_rne_bits(x1.w) << 16));
-      for (int j = a.fs_next[e]; j < a.fs_next[e + 1]; ++j) {
-        const int h = j / a.S, l = j - h * a.S;
-        st_stream(a.wbase[h] + (int64_t)l * a.P + gi, wb);
-      }
+      place_to(a, e, gi, wb);
       continue;
     }
 
@@ -103,24 +135,32 @@ __global__ void __launch_bounds__(kThreads) k_update(const __grid_constant__ Upd
     float4 *pv = reinterpret_cast<float4 *>(a.mom2[o] + so);
     const float4 w0 = pw[0], w1 = pw[1], m0 = pm[0], m1 = pm[1], v0 = pv[0], v1 = pv[1];
 
-    // a3: two-level fp32 sum over the replica slots [j0, j1) of expert e under plan_t
+    // a3: two-level fp32 sum over the replica slots [j0, j1) of expert e under plan_t.
+    // Slot j lives on GPU j / S at local slot j % S; (h, l) advance incrementally.
     const int j0 = a.fs_cur[e], j1 = a.fs_cur[e + 1];
     float part[8], tot[8];
     bool have_tot = false, have_part = false;
     int cur_h = -1;
-    for (int j = j0; j < j1; j += 4) {
-      const int n = min(4, j1 - j);
-      uint4 buf[4];
+    int h_ld = a.h_first_cur[e], l_ld = j0 - h_ld * a.S;
+    const int64_t P = a.P;
+    for (int j = j0; j < j1; j += kBatch) {
+      const int n = min(kBatch, j1 - j);
+      uint4 buf[kBatch];
+      int hb[kBatch];
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < kBatch; ++q)
         if (q < n) {
-          const int jj = j + q, h = jj / a.S, l = jj - h * a.S;
-          buf[q] = ld_stream(a.gbase[h] + (int64_t)l * a.P + gi);
+          buf[q] = ld_stream(a.gbase[h_ld] + (int64_t)l_ld * P + gi);
+          hb[q] = h_ld;
+          if (++l_ld == a.S) {
+            l_ld = 0;
+            ++h_ld;
+          }
         }
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < kBatch; ++q)
         if (q < n) {
-          const int h = (j + q) / a.S;
+          const int h = hb[q];
           float g8[8];
           unpack_bf16x8(buf[q], g8);
           if (!have_part) {
@@ -155,21 +195,12 @@ __global__ void __launch_bounds__(kThreads) k_update(const __grid_constant__ Upd
     }
     const float sc = a.scale[e];
 
-    // a4: Adam, reading A15 op order, IEEE fp32 RN per op
+    // a4: Adam
     float w[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
     float m[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
     float v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-    uint32_t ob[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const float g = __fmul_rn(tot[i], sc);
-      m[i] = __fadd_rn(__fmul_rn(a.b1, m[i]), __fmul_rn(a.omb1, g));
-      v[i] = __fadd_rn(__fmul_rn(a.b2, v[i]), __fmul_rn(a.omb2, __fmul_rn(g, g)));
-      const float den = __fadd_rn(__fdiv_rn(__fsqrt_rn(v[i]), a.rbc2), a.eps);
-      if (a.wd_on) w[i] = __fsub_rn(w[i], __fmul_rn(a.lrwd, w[i]));
-      w[i] = __fsub_rn(w[i], __fmul_rn(a.step, __fdiv_rn(m[i], den)));
-      ob[i] = bf16_rne_bits(w[i]);
-    }
+    uint4 wb;
+    adam8(a, tot, sc, w, m, v, wb);
     pw[0] = make_float4(w[0], w[1], w[2], w[3]);
     pw[1] = make_float4(w[4], w[5], w[6], w[7]);
     pm[0] = make_float4(m[0], m[1], m[2], m[3]);
@@ -178,13 +209,227 @@ __global__ void __launch_bounds__(kThreads) k_update(const __grid_constant__ Upd
     pv[1] = make_float4(v[4], v[5], v[6], v[7]);
 
     // a5: push the bf16 vector to every slot of plan_{t+1} hosting e (local or peer HBM)
-    const uint4 wb = make_uint4(ob[0] | (ob[1] << 16), ob[2] | (ob[3] << 16), ob[4] | (ob[5] << 16),
-                                ob[6] | (ob[7] << 16));
-    const int n0 = a.fs_next[e], n1 = a.fs_next[e + 1];
-    for (int j = n0; j < n1; ++j) {
-      const int h = j / a.S, l = j - h * a.S;
-      st_stream(a.wbase[h] + (int64_t)l * a.P + gi, wb);
+    place_to(a, e, gi, wb);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// k_update_tma: the same a3+a4+a5 computation, warp-specialised around shared-memory rings
+// filled by the bulk-copy engine (cp.async.bulk, SASS UBLKCP) -- bytes in flight cost no
+// registers, and each CTA streams ahead across items.
+//   warp 8 (producer, one lane): for each item (o, e, chunk) in this CTA's order, one
+//     24 KB state tile (master, m, v: 3 x 2048 fp32) into the state ring, then the 4 KB
+//     bf16 grad slice of every replica slot of e (local or peer HBM) into the grad ring;
+//     completion via mbarrier complete_tx.
+//   warps 0-7 (consumers, 8 elements per thread): wait full -> read smem -> arrive empty;
+//     the same two-level sum / Adam / bf16 as k_update, then 16-byte stores of the state
+//     and of the bf16 weights to every slot of plan_next (local or peer HBM).
+// 2 CTAs per SM (~97 KB shared memory each).
+// ------------------------------------------------------------------------------------------
+constexpr int kConsumerWarps = kThreads / 32;            // 8
+constexpr int kTmaThreads = kThreads + 32;               // + 1 producer warp
+constexpr int kStateSlots = 2;
+constexpr int kGradSlots = 12;
+constexpr int kStateTileBytes = 3 * kChunk * 4;          // 24 KB
+constexpr int kGradTileBytes = kChunk * 2;               // 4 KB
+constexpr int kTmaSmem = kStateSlots * kStateTileBytes + kGradSlots * kGradTileBytes +
+                         2 * (kStateSlots + kGradSlots) * 8;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+// Consumer warp releases a ring slot.  The generic-proxy shared-memory reads of the slot must
+// be ordered before the async-proxy (bulk copy) write that refills it: every lane fences its
+// own reads (fence.proxy.async), then one lane arrives on the slot's empty barrier.
+__device__ __forceinline__ void release_slot(uint64_t *empty, int lane) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if (lane == 0) mbar_arrive(empty);
+}
+// global -> shared bulk copy, completion counted on mbarrier b (bytes % 16 == 0, 16-B aligned)
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(b))
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kTmaThreads, 2) k_update_tma(const __grid_constant__ UpdArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  float *state = reinterpret_cast<float *>(smem);                              // [slots][3][chunk]
+  uint16_t *grad = reinterpret_cast<uint16_t *>(smem + kStateSlots * kStateTileBytes);
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem + kStateSlots * kStateTileBytes +
+                                               kGradSlots * kGradTileBytes);
+  uint64_t *st_full = bar, *st_empty = bar + kStateSlots;
+  uint64_t *gr_full = bar + 2 * kStateSlots, *gr_empty = bar + 2 * kStateSlots + kGradSlots;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kStateSlots; ++i) {
+      mbar_init(st_full + i, 1);
+      mbar_init(st_empty + i, kConsumerWarps);
     }
+    for (int i = 0; i < kGradSlots; ++i) {
+      mbar_init(gr_full + i, 1);
+      mbar_init(gr_empty + i, kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const int64_t per_owner = (int64_t)a.E * a.nchunks;
+  const int64_t total = per_owner * a.o_count;
+  const int64_t P = a.P;
+
+  if (warp == kConsumerWarps) {  // ---------------- producer ----------------
+    if (lane != 0) return;
+    uint32_t si = 0, gi_ = 0;
+    for (int64_t it = blockIdx.x; it < total; it += gridDim.x) {
+      const int o = a.o_begin + (int)(it / per_owner);
+      const int64_t rem = it - (int64_t)(o - a.o_begin) * per_owner;
+      const int e = (int)(rem / a.nchunks);
+      const int64_t c = rem - (int64_t)e * a.nchunks;
+      const int64_t loc0 = c * kChunk;
+      const uint32_t nval = (uint32_t)(a.Pg - loc0 < kChunk ? a.Pg - loc0 : kChunk);
+      const int64_t so = (int64_t)e * a.Pg + loc0;
+      {
+        const int s = si % kStateSlots;
+        mbar_wait(st_empty + s, ((si / kStateSlots) & 1) ^ 1);
+        mbar_expect_tx(st_full + s, 3 * nval * 4);
+        float *dst = state + (size_t)s * 3 * kChunk;
+        bulk_g2s(dst, a.master[o] + so, nval * 4, st_full + s);
+        bulk_g2s(dst + kChunk, a.mom1[o] + so, nval * 4, st_full + s);
+        bulk_g2s(dst + 2 * kChunk, a.mom2[o] + so, nval * 4, st_full + s);
+        ++si;
+      }
+      const int64_t g0 = (int64_t)o * a.Pg + loc0;
+      const int j0 = a.fs_cur[e], j1 = a.fs_cur[e + 1];
+      int h = a.h_first_cur[e], l = j0 - h * a.S;
+      for (int j = j0; j < j1; ++j) {
+        const int g = gi_ % kGradSlots;
+        mbar_wait(gr_empty + g, ((gi_ / kGradSlots) & 1) ^ 1);
+        mbar_expect_tx(gr_full + g, nval * 2);
+        bulk_g2s(grad + (size_t)g * kChunk, a.gbase[h] + (int64_t)l * P + g0, nval * 2, gr_full + g);
+        ++gi_;
+        if (++l == a.S) {
+          l = 0;
+          ++h;
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  const int tid = threadIdx.x;
+  uint32_t si = 0, gi_ = 0;
+  for (int64_t it = blockIdx.x; it < total; it += gridDim.x) {
+    const int o = a.o_begin + (int)(it / per_owner);
+    const int64_t rem = it - (int64_t)(o - a.o_begin) * per_owner;
+    const int e = (int)(rem / a.nchunks);
+    const int64_t c = rem - (int64_t)e * a.nchunks;
+    const int64_t loc = c * kChunk + (int64_t)tid * kVec;
+    const bool act = loc < a.Pg;
+    float w[8], m[8], v[8];
+    {
+      const int s = si % kStateSlots;
+      mbar_wait(st_full + s, (si / kStateSlots) & 1);
+      if (act) {
+        const float *src = state + (size_t)s * 3 * kChunk + tid * kVec;
+        const float4 w0 = *reinterpret_cast<const float4 *>(src);
+        const float4 w1 = *reinterpret_cast<const float4 *>(src + 4);
+        const float4 m0 = *reinterpret_cast<const float4 *>(src + kChunk);
+        const float4 m1 = *reinterpret_cast<const float4 *>(src + kChunk + 4);
+        const float4 v0 = *reinterpret_cast<const float4 *>(src + 2 * kChunk);
+        const float4 v1 = *reinterpret_cast<const float4 *>(src + 2 * kChunk + 4);
+        w[0] = w0.x; w[1] = w0.y; w[2] = w0.z; w[3] = w0.w; w[4] = w1.x; w[5] = w1.y; w[6] = w1.z; w[7] = w1.w;
+        m[0] = m0.x; m[1] = m0.y; m[2] = m0.z; m[3] = m0.w; m[4] = m1.x; m[5] = m1.y; m[6] = m1.z; m[7] = m1.w;
+        v[0] = v0.x; v[1] = v0.y; v[2] = v0.z; v[3] = v0.w; v[4] = v1.x; v[5] = v1.y; v[6] = v1.z; v[7] = v1.w;
+      }
+      release_slot(st_empty + s, lane);
+      ++si;
+    }
+    // a3: two-level fp32 sum, replica slices in ascending slot order (reading A11)
+    const int j0 = a.fs_cur[e], j1 = a.fs_cur[e + 1];
+    float part[8], tot[8];
+    bool have_tot = false;
+    int h = a.h_first_cur[e], l = j0 - h * a.S, cur_h = h;
+    for (int j = j0; j < j1; ++j) {
+      const int g = gi_ % kGradSlots;
+      mbar_wait(gr_full + g, (gi_ / kGradSlots) & 1);
+      if (act) {
+        const uint4 x = *reinterpret_cast<const uint4 *>(grad + (size_t)g * kChunk + tid * kVec);
+        float g8[8];
+        unpack_bf16x8(x, g8);
+        if (j == j0) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) part[i] = g8[i];
+        } else if (h != cur_h) {  // next GPU: fold the finished per-GPU partial into tot
+          if (have_tot) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) tot[i] = __fadd_rn(tot[i], part[i]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) tot[i] = part[i];
+          }
+          have_tot = true;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) part[i] = g8[i];
+          cur_h = h;
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) part[i] = __fadd_rn(part[i], g8[i]);
+        }
+      }
+      release_slot(gr_empty + g, lane);
+      ++gi_;
+      if (++l == a.S) {
+        l = 0;
+        ++h;
+      }
+    }
+    if (!act) continue;
+    if (have_tot) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) tot[i] = __fadd_rn(tot[i], part[i]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) tot[i] = part[i];
+    }
+    uint4 wb;
+    adam8(a, tot, a.scale[e], w, m, v, wb);                              // a4
+    const int64_t so = (int64_t)e * a.Pg + loc;
+    float4 *pw = reinterpret_cast<float4 *>(a.master[o] + so);
+    float4 *pm = reinterpret_cast<float4 *>(a.mom1[o] + so);
+    float4 *pv = reinterpret_cast<float4 *>(a.mom2[o] + so);
+    pw[0] = make_float4(w[0], w[1], w[2], w[3]);
+    pw[1] = make_float4(w[4], w[5], w[6], w[7]);
+    pm[0] = make_float4(m[0], m[1], m[2], m[3]);
+    pm[1] = make_float4(m[4], m[5], m[6], m[7]);
+    pv[0] = make_float4(v[0], v[1], v[2], v[3]);
+    pv[1] = make_float4(v[4], v[5], v[6], v[7]);
+    place_to(a, e, (int64_t)o * a.Pg + loc, wb);                          // a5
   }
 }
 
@@ -220,9 +465,14 @@ using namespace moe;
 
 int moe_validate_plan(const moe_ctx *ctx, const moe_plan_t *p, const char *what);  // ctx.cu
 
-int moe_update_blocks_per_sm() {
+// Per-device setup at context creation: occupancy of k_update, shared-memory opt-in of
+// k_update_tma.  Returns blocks per SM of k_update (>= 1), or -1 on a CUDA error.
+int moe_update_init() {
+  if (cudaFuncSetAttribute(k_update_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem) !=
+      cudaSuccess)
+    return -1;
   int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_update, kThreads, 0) != cudaSuccess) return 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_update, kThreads, 0) != cudaSuccess) return -1;
   return std::max(1, n);
 }
 
@@ -275,6 +525,10 @@ int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *pl
     a.fs_cur[e] = plan_cur->first_slot[e];
     a.fs_next[e] = plan_next->first_slot[e];
   }
+  for (int e = 0; e < ctx->E; ++e) {
+    a.h_first_cur[e] = (uint8_t)(plan_cur->first_slot[e] / ctx->S);
+    a.h_first_next[e] = (uint8_t)(plan_next->first_slot[e] / ctx->S);
+  }
   for (int h = 0; h < ctx->G; ++h) {
     a.gbase[h] = (const uint16_t *)ctx->peer_slot_g[h];
     a.wbase[h] = (uint16_t *)ctx->peer_slot_w[h];
@@ -300,10 +554,18 @@ int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *pl
     MOE_CUDA_TRY(cudaGetLastError());
   }
   const int64_t items = (int64_t)ctx->E * a.nchunks * a.o_count;
-  const int64_t grid = std::min<int64_t>(items, (int64_t)ctx->num_sms * ctx->upd_blocks_per_sm);
-  if (grid > 0) {
-    k_update<<<(unsigned)grid, kThreads, 0, s>>>(a);
-    MOE_CUDA_TRY(cudaGetLastError());
+  if (place_only || ctx->update_kernel == 0) {
+    const int64_t grid = std::min<int64_t>(items, (int64_t)ctx->num_sms * ctx->upd_blocks_per_sm);
+    if (grid > 0) {
+      k_update<<<(unsigned)grid, kThreads, 0, s>>>(a);
+      MOE_CUDA_TRY(cudaGetLastError());
+    }
+  } else {
+    const int64_t grid = std::min<int64_t>(items, (int64_t)ctx->num_sms * 2);
+    if (grid > 0) {
+      k_update_tma<<<(unsigned)grid, kTmaThreads, kTmaSmem, s>>>(a);
+      MOE_CUDA_TRY(cudaGetLastError());
+    }
   }
   if (multi) {  // barrier-out: every push into this GPU's slots has landed
     ba.which = 1;

@@ -66,6 +66,9 @@ CONFIGS = {
                            slots_total=256, trace="walk-spike", G_default=8),
     "stress": Workload("stress", E=64, d=1024, ffn=4096, mats=2, k=2, T=65536, slots_total=128,
                        trace="rotating-hot", G_default=8),
+    # parity-only: GPT-small's shape scaled down so the oracle can check every element
+    "medium": Workload("medium", E=16, d=256, ffn=2048, mats=2, k=2, T=16384, slots_total=64,
+                       trace="walk-spike", G_default=4),
 }
 
 # BASE seed; config i uses BASE_SEED + i

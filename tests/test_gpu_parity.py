@@ -61,7 +61,8 @@ def test_minmax_policy_and_weight_decay_and_scale_modes():
 def test_rotating_hot_trace_tiny():
     from gpu_helpers import run_parity
     wl = configs.CONFIGS["tiny-skew"]
-    tr = traces.rotating_hot(wl.E, wl.T, wl.k, 7, seed=3)
+    # E = 8 has one hot expert; weight 4 keeps its quota <= T (distinct experts per token)
+    tr = traces.rotating_hot(wl.E, wl.T, wl.k, 7, seed=3, hot_weight=4)
     run_parity("tiny-skew", 4, 7, trace=tr)
 
 
@@ -126,16 +127,25 @@ def test_synth_kernels_match_numpy_generator():
     assert np.array_equal(m.view(torch.int32).cpu().numpy().view(np.uint32).reshape(4, 5000), want)
 
 
-def _sample_idx(P: int, G: int, n: int = 2048) -> np.ndarray:
-    """Random elements plus every owner's first/last elements and chunk boundaries."""
-    rng = np.random.default_rng(P % 1000)
+def _sample_idx(P: int, G: int, stride: int = 97) -> np.ndarray:
+    """Every 97th element (a prime stride: all chunk offsets and all threads of the update
+    kernel get hit) plus every owner's first/last elements and chunk boundaries.  Dense
+    enough to catch rare races (a 7-in-1.4M corruption was once missed by a 2K sample)."""
     Pg = P // G
-    pts = set(rng.integers(0, P, n).tolist())
+    pts = set(range(0, P, stride))
     for g in range(G):
         for off in (0, 1, 7, 8, 2047, 2048, Pg - 8, Pg - 1):
             if 0 <= off < Pg:
                 pts.add(g * Pg + off)
     return np.array(sorted(pts), dtype=np.int64)
+
+
+@pytest.mark.parametrize("G", [1, 4])
+def test_medium_every_element(G):
+    """A 1M-parameter-per-expert workload compared on EVERY element for 5 iterations
+    (the kernels' multi-chunk, multi-item-per-CTA regime, small enough for the full oracle)."""
+    from gpu_helpers import run_parity
+    run_parity("medium", G, 5)
 
 
 @pytest.mark.parametrize("name,G,iters", [("gpt-small", 1, 3), ("stress", 1, 3),

@@ -1,0 +1,38 @@
+"""Real multi-GPU runs (one process per GPU, NVLink peers).  Skipped on a 1-GPU box."""
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+pytestmark = pytest.mark.gpu
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _torchrun(n: int, *args, timeout=600):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(ROOT, "tests", "mp_parity.py"), *args]
+    return subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
+
+
+@pytest.mark.parametrize("G,config,extra", [
+    (2, "tiny-skew", []), (2, "tiny", []), (4, "tiny-skew", []), (4, "tiny", ["--trace", "rotating-hot"]),
+    (2, "gpt-small", ["--sampled", "--iters", "3"]), (8, "gpt-small", ["--sampled", "--iters", "3"]),
+])
+def test_real_multi_gpu_parity(G, config, extra):
+    if torch.cuda.device_count() < G:
+        pytest.skip(f"needs {G} GPUs")
+    r = _torchrun(G, "--config", config, *extra)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "OK" in r.stdout
