@@ -71,6 +71,7 @@ void free_ctx(moe_ctx *c) {
   cudaFree(c->einfo);
   cudaFree(c->counts_dev);
   cudaFree(c->err);
+  cudaFree(c->item_ctr);
   if (c->counts_ev) cudaEventDestroy(c->counts_ev);
   delete c;
 }
@@ -125,6 +126,7 @@ extern "C" int moe_ctx_create(const moe_ctx_desc *d, moe_ctx **out) {
   c->einfo = nullptr;
   c->counts_dev = nullptr;
   c->err = nullptr;
+  c->item_ctr = nullptr;
   c->counts_ev = nullptr;
   c->counts_pending = false;
   for (int v = 0; v < n_local; ++v) {
@@ -147,12 +149,14 @@ extern "C" int moe_ctx_create(const moe_ctx_desc *d, moe_ctx **out) {
   chk(cudaMalloc(&c->einfo, sizeof(ExpertInfo) * n_local * c->E));
   chk(cudaMalloc(&c->counts_dev, sizeof(int64_t) * c->E));
   chk(cudaMalloc(&c->err, sizeof(int32_t)));
+  chk(cudaMalloc(&c->item_ctr, 2 * sizeof(unsigned long long)));
   chk(cudaEventCreateWithFlags(&c->counts_ev, cudaEventDisableTiming));
   if (e == cudaSuccess) {
     chk(cudaMemset(c->sync, 0, sizeof(SyncBuf)));
     chk(cudaMemset(c->cnt_local, 0, sizeof(int32_t) * n_local * c->E));
     chk(cudaMemset(c->done, 0, sizeof(uint32_t) * n_local));
     chk(cudaMemset(c->err, 0, sizeof(int32_t)));
+    chk(cudaMemset(c->item_ctr, 0, 2 * sizeof(unsigned long long)));
     chk(cudaDeviceSynchronize());
   }
   if (e != cudaSuccess) {

@@ -75,6 +75,7 @@ struct moe_ctx {
   moe::ExpertInfo *einfo;   // [n_local][E]
   int64_t *counts_dev;      // [E]
   int32_t *err;             // device error bits
+  unsigned long long *item_ctr;  // [2] dynamic-scheduling counters of k_update_tma (self-resetting)
   int64_t nb_max;
   cudaEvent_t counts_ev;    // recorded after the C_e device->host copy
   bool counts_pending;

@@ -44,6 +44,7 @@ struct UpdArgs {
   float *master[MOE_MAX_G];          // fp32 [E][Pg], per owner
   float *mom1[MOE_MAX_G];
   float *mom2[MOE_MAX_G];
+  unsigned long long *item_ctr;  // [2] k_update_tma work counter + finished-CTA counter (zero between launches)
 };
 
 __device__ __forceinline__ uint4 ld_stream(const uint16_t *p) {
@@ -74,6 +75,13 @@ __device__ __forceinline__ uint32_t bf16_rne_bits(float x) {
 }
 
 constexpr int kBatch = 8;  // replica grad slices loaded per round (16 B each, in flight together)
+
+// kItemOrder note: work items (owner o, expert e, chunk c) are enumerated CHUNK-major
+// (it = (o * nchunks + c) * E + e).  All CTAs of all GPUs then work on every expert at
+// once, so the NVLink pulls (from the GPUs holding plan_cur's replicas) and pushes (to
+// plan_next's replicas) are spread over all peers at every instant.  Expert-major order made
+// every GPU hit the same one or two GPUs hosting the current expert (incast), capping NVLink
+// at ~46 % of a link at G = 4 even though the total per-GPU volume is balanced (App. E).
 
 // a5: the 16-byte bf16 vector -> every slot j of plan_next hosting e; slot j is on GPU j / S.
 __device__ __forceinline__ void place_to(const UpdArgs &a, int e, int64_t gi, const uint4 &wb) {
@@ -112,8 +120,8 @@ __global__ void __launch_bounds__(kThreads) k_update(const __grid_constant__ Upd
   for (int64_t it = blockIdx.x; it < total; it += gridDim.x) {
     const int o = a.o_begin + (int)(it / per_owner);
     const int64_t rem = it - (int64_t)(o - a.o_begin) * per_owner;
-    const int e = (int)(rem / a.nchunks);
-    const int64_t c = rem - (int64_t)e * a.nchunks;
+    const int e = (int)(rem % a.E);  // chunk-major item order (see kItemOrder note)
+    const int64_t c = rem / a.E;
     const int64_t loc = c * kChunk + (int64_t)threadIdx.x * kVec;
     if (loc >= a.Pg) continue;
     const int64_t gi = (int64_t)o * a.Pg + loc;  // element index inside the expert
@@ -233,7 +241,7 @@ constexpr int kGradSlots = 12;
 constexpr int kStateTileBytes = 3 * kChunk * 4;          // 24 KB
 constexpr int kGradTileBytes = kChunk * 2;               // 4 KB
 constexpr int kTmaSmem = kStateSlots * kStateTileBytes + kGradSlots * kGradTileBytes +
-                         2 * (kStateSlots + kGradSlots) * 8;
+                         2 * (kStateSlots + kGradSlots) * 8 + kStateSlots * 8;  // + slot item ids
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -284,6 +292,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_update_tma(const __grid_cons
                                                kGradSlots * kGradTileBytes);
   uint64_t *st_full = bar, *st_empty = bar + kStateSlots;
   uint64_t *gr_full = bar + 2 * kStateSlots, *gr_empty = bar + 2 * kStateSlots + kGradSlots;
+  volatile int64_t *slot_item = reinterpret_cast<volatile int64_t *>(bar + 2 * (kStateSlots + kGradSlots));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStateSlots; ++i) {
@@ -305,17 +314,32 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_update_tma(const __grid_cons
   if (warp == kConsumerWarps) {  // ---------------- producer ----------------
     if (lane != 0) return;
     uint32_t si = 0, gi_ = 0;
-    for (int64_t it = blockIdx.x; it < total; it += gridDim.x) {
+    for (;;) {
+      // dynamic scheduling: claim the next item (chunk-major order, see kItemOrder note)
+      const int64_t it = (int64_t)atomicAdd(a.item_ctr, 1ull);
+      const int s = si % kStateSlots;
+      mbar_wait(st_empty + s, ((si / kStateSlots) & 1) ^ 1);
+      if (it >= total) {  // no more work: hand the consumers a sentinel
+        slot_item[s] = -1;
+        mbar_arrive(st_full + s);
+        // the last producer to finish resets the counters for the next launch (every other
+        // producer has already made its final, failing claim)
+        if (atomicAdd(a.item_ctr + 1, 1ull) == gridDim.x - 1) {
+          a.item_ctr[0] = 0;
+          a.item_ctr[1] = 0;
+          __threadfence();
+        }
+        break;
+      }
+      slot_item[s] = it;
       const int o = a.o_begin + (int)(it / per_owner);
       const int64_t rem = it - (int64_t)(o - a.o_begin) * per_owner;
-      const int e = (int)(rem / a.nchunks);
-      const int64_t c = rem - (int64_t)e * a.nchunks;
+      const int e = (int)(rem % a.E);
+      const int64_t c = rem / a.E;
       const int64_t loc0 = c * kChunk;
       const uint32_t nval = (uint32_t)(a.Pg - loc0 < kChunk ? a.Pg - loc0 : kChunk);
       const int64_t so = (int64_t)e * a.Pg + loc0;
       {
-        const int s = si % kStateSlots;
-        mbar_wait(st_empty + s, ((si / kStateSlots) & 1) ^ 1);
         mbar_expect_tx(st_full + s, 3 * nval * 4);
         float *dst = state + (size_t)s * 3 * kChunk;
         bulk_g2s(dst, a.master[o] + so, nval * 4, st_full + s);
@@ -344,17 +368,19 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_update_tma(const __grid_cons
   // ---------------- consumers ----------------
   const int tid = threadIdx.x;
   uint32_t si = 0, gi_ = 0;
-  for (int64_t it = blockIdx.x; it < total; it += gridDim.x) {
+  for (;;) {
+    const int s = si % kStateSlots;
+    mbar_wait(st_full + s, (si / kStateSlots) & 1);
+    const int64_t it = slot_item[s];
+    if (it < 0) break;
     const int o = a.o_begin + (int)(it / per_owner);
     const int64_t rem = it - (int64_t)(o - a.o_begin) * per_owner;
-    const int e = (int)(rem / a.nchunks);
-    const int64_t c = rem - (int64_t)e * a.nchunks;
+    const int e = (int)(rem % a.E);
+    const int64_t c = rem / a.E;
     const int64_t loc = c * kChunk + (int64_t)tid * kVec;
     const bool act = loc < a.Pg;
     float w[8], m[8], v[8];
     {
-      const int s = si % kStateSlots;
-      mbar_wait(st_full + s, (si / kStateSlots) & 1);
       if (act) {
         const float *src = state + (size_t)s * 3 * kChunk + tid * kVec;
         const float4 w0 = *reinterpret_cast<const float4 *>(src);
@@ -539,6 +565,7 @@ int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *pl
     a.mom1[o] = ctx->adam_m[v];
     a.mom2[o] = ctx->adam_v[v];
   }
+  a.item_ctr = ctx->item_ctr;
   const bool multi = ctx->rank >= 0 && ctx->G > 1;
   const uint32_t epoch = ++ctx->upd_epoch;
   BarrierArgs ba{};
