@@ -144,6 +144,14 @@ int moe_ctx_export(moe_ctx *ctx, void *out);
  * must connect before any rank's first moe_dispatch / moe_update.               */
 int moe_ctx_connect(moe_ctx *ctx, const void *all);
 
+/* Measurement hooks.  While enabled, the library records CUDA events on the launching stream
+ * around each dispatch (its three kernels) and around each update kernel launch (excluding
+ * the cross-GPU barriers).  moe_ctx_get_timing synchronises on the recorded events, returns
+ * the summed milliseconds and launch counts since the previous call, and clears them.      */
+int moe_ctx_set_timing(moe_ctx *ctx, int32_t enable);
+int moe_ctx_get_timing(moe_ctx *ctx, double *dispatch_ms, int64_t *n_dispatch, double *update_ms,
+                       int64_t *n_update);
+
 /* Synchronises `stream`, then reports and clears device-raised errors
  * (MOE_ERR_DATA, MOE_ERR_TIMEOUT).                                               */
 int moe_ctx_check(moe_ctx *ctx, void *stream);
@@ -199,6 +207,22 @@ typedef struct {
 
 int moe_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *plan_next,
                const moe_adam_t *adam, void *stream);
+
+/* ------------------------------------------------------------------------------------------
+ * One whole iteration, natively, in the paper's order (fig:design_diagram):
+ *   moe_dispatch(plan_cur)                                   a0 + a2   (device, async)
+ *   wait for C_t in out->counts_host (pinned; required)     (host spins on a pinned flag that
+ *                                                             the scan kernel releases; the
+ *                                                             scatter kernel keeps running)
+ *   moe_plan_ex(C_t, policy) -> *plan_next                   a1        (host C++; "may execute
+ *                                                             earlier, even right after
+ *                                                             step 1", PAPER.md:709 fn)
+ *   moe_update(plan_cur, plan_next, adam)                    a3+a4+a5  (device, async)
+ * plan_next: caller-allocated arrays, filled here.  Returns after the update is enqueued.
+ * Errors: those of the four calls; MOE_ERR_INVALID if out->counts_host is NULL.           */
+int moe_step(moe_ctx *ctx, const int32_t *topk_ids, const float *gates, int64_t T,
+             const moe_plan_t *plan_cur, moe_plan_t *plan_next, int32_t policy,
+             const moe_dispatch_out *out, const moe_adam_t *adam, void *stream);
 
 /* a5 alone: writes bf16 RNE of the owners' current fp32 master shards into every slot of
  * `plan`.  Used to materialise the initial placement plan_0 (and after a

@@ -8,5 +8,5 @@ library raises.
 """
 from .api import (AdamConfig, DispatchBuffers, MoeContext, MoeError, Plan,  # noqa: F401
                   MOE_PLAN_MINMAX, MOE_PLAN_PAPER_ALG1, moe_dispatch, moe_place, moe_plan,
-                  moe_update, synth_grads, synth_master)
+                  moe_step, moe_update, synth_grads, synth_master)
 from .layer import DecoupledExpertLayer  # noqa: F401

@@ -23,7 +23,7 @@ OUT = os.path.join(HERE, "libmoedc.so")
 OBJ = os.path.join(HERE, "build")
 
 CU = ["ctx.cu", "dispatch.cu", "update.cu", "synth.cu"]
-CPP = ["plan.cpp"]
+CPP = ["plan.cpp", "step.cpp"]
 HEADERS = [os.path.join(CSRC, h) for h in ("common.h", "internal.h")] + \
     [os.path.join(INC, h) for h in ("moe_dc.h", "moe_synth.h")]
 

@@ -22,7 +22,7 @@ EXPORTED = [
     "moe_status_str", "moe_last_error", "moe_abi_version", "moe_plan", "moe_plan_ex",
     "moe_ctx_create", "moe_ctx_destroy", "moe_ctx_handle_bytes", "moe_ctx_export",
     "moe_ctx_connect", "moe_ctx_check", "moe_ctx_wait_counts", "moe_dispatch", "moe_update",
-    "moe_place",
+    "moe_place", "moe_step", "moe_ctx_set_timing", "moe_ctx_get_timing",
     "moe_synth_grads", "moe_synth_master",
 ]
 
@@ -96,6 +96,15 @@ def lib() -> C.CDLL:
         L.moe_dispatch.restype = C.c_int
         L.moe_dispatch.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                                    C.POINTER(MoePlanT), C.POINTER(MoeDispatchOut), C.c_void_p]
+        L.moe_step.restype = C.c_int
+        L.moe_step.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(MoePlanT),
+                               C.POINTER(MoePlanT), C.c_int32, C.POINTER(MoeDispatchOut),
+                               C.POINTER(MoeAdamT), C.c_void_p]
+        L.moe_ctx_set_timing.restype = C.c_int
+        L.moe_ctx_set_timing.argtypes = [C.c_void_p, C.c_int32]
+        L.moe_ctx_get_timing.restype = C.c_int
+        L.moe_ctx_get_timing.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64),
+                                         C.POINTER(C.c_double), C.POINTER(C.c_int64)]
         L.moe_update.restype = C.c_int
         L.moe_update.argtypes = [C.c_void_p, C.POINTER(MoePlanT), C.POINTER(MoePlanT),
                                  C.POINTER(MoeAdamT), C.c_void_p]

@@ -137,6 +137,18 @@ class MoeContext:
         """Exchange the CUDA-IPC records over a torch.distributed group and map the peers."""
         self.connect(gather_records(self.export(), self.G, group))
 
+    def set_timing(self, enable: bool) -> None:
+        check(L.lib().moe_ctx_set_timing(self.handle, int(enable)), "moe_ctx_set_timing")
+
+    def get_timing(self) -> dict:
+        """Summed CUDA-event ms and launch counts of dispatches / update kernels since last call."""
+        dm, um = C.c_double(), C.c_double()
+        dn, un = C.c_int64(), C.c_int64()
+        check(L.lib().moe_ctx_get_timing(self.handle, C.byref(dm), C.byref(dn), C.byref(um),
+                                         C.byref(un)), "moe_ctx_get_timing")
+        return {"dispatch_ms": dm.value, "n_dispatch": dn.value, "update_ms": um.value,
+                "n_update": un.value}
+
     def wait_counts(self) -> None:
         """Host waits for the C_e copy of the last moe_dispatch (not for its scatter)."""
         check(L.lib().moe_ctx_wait_counts(self.handle), "moe_ctx_wait_counts")
@@ -213,6 +225,26 @@ def moe_update(ctx: MoeContext, plan_cur: Plan, plan_next: Plan, adam: AdamConfi
                    sc.ctypes.data_as(C.POINTER(C.c_float)) if sc is not None else None)
     check(L.lib().moe_update(ctx.handle, C.byref(plan_cur.c), C.byref(plan_next.c), C.byref(a),
                              _stream_ptr(stream)), "moe_update")
+
+
+def moe_step(ctx: MoeContext, topk_ids: torch.Tensor, gates: torch.Tensor, T: int, plan_cur: Plan,
+             policy: int, out: DispatchBuffers, adam: AdamConfig, step: int, scale_mode: int = 0,
+             scale=None, stream=None) -> Plan:
+    """a0..a5 in one native call (dispatch -> host plan -> update); returns plan_{t+1}."""
+    if topk_ids.dtype != torch.int32 or gates.dtype != torch.float32:
+        raise ValueError("topk_ids int32, gates fp32")
+    if topk_ids.numel() != ctx.n_local * T * ctx.k or gates.numel() != topk_ids.numel():
+        raise ValueError("topk_ids/gates must hold n_local*T*k elements")
+    if out.T < T:
+        raise ValueError("DispatchBuffers too small")
+    nxt = Plan(ctx.E, ctx.G, ctx.S)
+    sc = None if scale is None else np.ascontiguousarray(scale, dtype=np.float32)
+    a = L.MoeAdamT(adam.lr, adam.beta1, adam.beta2, adam.eps, adam.weight_decay, step, scale_mode,
+                   sc.ctypes.data_as(C.POINTER(C.c_float)) if sc is not None else None)
+    check(L.lib().moe_step(ctx.handle, _ptr(topk_ids), _ptr(gates), T, C.byref(plan_cur.c),
+                           C.byref(nxt.c), policy, C.byref(out.c), C.byref(a), _stream_ptr(stream)),
+          "moe_step")
+    return nxt
 
 
 def moe_place(ctx: MoeContext, plan: Plan, stream=None) -> None:

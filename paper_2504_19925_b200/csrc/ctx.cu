@@ -11,6 +11,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
+#include <atomic>
+#include <chrono>
 #include <cstring>
 #include <string>
 
@@ -72,7 +75,13 @@ void free_ctx(moe_ctx *c) {
   cudaFree(c->counts_dev);
   cudaFree(c->err);
   cudaFree(c->item_ctr);
-  if (c->counts_ev) cudaEventDestroy(c->counts_ev);
+  cudaFree(c->scan_done);
+  if (c->host_flag) cudaFreeHost((void *)c->host_flag);
+  for (auto *v : {&c->ev_pool, &c->ev_disp, &c->ev_upd})
+    for (auto &p : *v) {
+      cudaEventDestroy(p.first);
+      cudaEventDestroy(p.second);
+    }
   delete c;
 }
 
@@ -127,8 +136,11 @@ extern "C" int moe_ctx_create(const moe_ctx_desc *d, moe_ctx **out) {
   c->counts_dev = nullptr;
   c->err = nullptr;
   c->item_ctr = nullptr;
-  c->counts_ev = nullptr;
+  c->scan_done = nullptr;
+  c->host_flag = nullptr;
+  c->host_flag_dev = nullptr;
   c->counts_pending = false;
+  c->timing = false;
   for (int v = 0; v < n_local; ++v) {
     c->slot_w.push_back(d->slot_w[v]);
     c->slot_g.push_back(d->slot_g[v]);
@@ -150,13 +162,25 @@ extern "C" int moe_ctx_create(const moe_ctx_desc *d, moe_ctx **out) {
   chk(cudaMalloc(&c->counts_dev, sizeof(int64_t) * c->E));
   chk(cudaMalloc(&c->err, sizeof(int32_t)));
   chk(cudaMalloc(&c->item_ctr, 2 * sizeof(unsigned long long)));
-  chk(cudaEventCreateWithFlags(&c->counts_ev, cudaEventDisableTiming));
+  chk(cudaMalloc(&c->scan_done, sizeof(uint32_t)));
+  {
+    void *hf = nullptr;
+    chk(cudaHostAlloc(&hf, sizeof(uint32_t), cudaHostAllocMapped));
+    c->host_flag = (volatile uint32_t *)hf;
+    if (hf) {
+      *c->host_flag = 0;
+      void *dp = nullptr;
+      chk(cudaHostGetDevicePointer(&dp, hf, 0));
+      c->host_flag_dev = (uint32_t *)dp;
+    }
+  }
   if (e == cudaSuccess) {
     chk(cudaMemset(c->sync, 0, sizeof(SyncBuf)));
     chk(cudaMemset(c->cnt_local, 0, sizeof(int32_t) * n_local * c->E));
     chk(cudaMemset(c->done, 0, sizeof(uint32_t) * n_local));
     chk(cudaMemset(c->err, 0, sizeof(int32_t)));
     chk(cudaMemset(c->item_ctr, 0, 2 * sizeof(unsigned long long)));
+    chk(cudaMemset(c->scan_done, 0, sizeof(uint32_t)));
     chk(cudaDeviceSynchronize());
   }
   if (e != cudaSuccess) {
@@ -252,7 +276,50 @@ extern "C" int moe_ctx_connect(moe_ctx *ctx, const void *all) {
 extern "C" int moe_ctx_wait_counts(moe_ctx *ctx) {
   if (!ctx) return fail(MOE_ERR_INVALID, "moe_ctx_wait_counts: NULL ctx");
   if (!ctx->counts_pending) return MOE_OK;
-  MOE_CUDA_TRY(cudaEventSynchronize(ctx->counts_ev));
+  // spin on the pinned flag k_scan releases (system scope) once C_e is in host memory
+  const uint32_t want = ctx->disp_epoch;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (uint64_t n = 0; (int32_t)(*ctx->host_flag - want) < 0; ++n) {
+    if ((n & 1023) == 0) {
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(30))
+        return fail(MOE_ERR_TIMEOUT, "moe_ctx_wait_counts: C_e never arrived (dispatch failed?)");
+      cudaError_t e = cudaPeekAtLastError();
+      if (e != cudaSuccess) return fail(MOE_ERR_CUDA, "moe_ctx_wait_counts: %s", cudaGetErrorString(e));
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+  ctx->counts_pending = false;
+  return MOE_OK;
+}
+
+extern "C" int moe_ctx_set_timing(moe_ctx *ctx, int32_t enable) {
+  if (!ctx) return fail(MOE_ERR_INVALID, "moe_ctx_set_timing: NULL ctx");
+  ctx->timing = enable != 0;
+  return MOE_OK;
+}
+
+extern "C" int moe_ctx_get_timing(moe_ctx *ctx, double *dispatch_ms, int64_t *n_dispatch,
+                                  double *update_ms, int64_t *n_update) {
+  if (!ctx) return fail(MOE_ERR_INVALID, "moe_ctx_get_timing: NULL ctx");
+  MOE_CUDA_TRY(cudaSetDevice(ctx->device));
+  double sums[2] = {0.0, 0.0};
+  int64_t counts[2] = {0, 0};
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> *lists[2] = {&ctx->ev_disp, &ctx->ev_upd};
+  for (int k = 0; k < 2; ++k) {
+    for (auto &p : *lists[k]) {
+      float ms = 0.f;
+      MOE_CUDA_TRY(cudaEventSynchronize(p.second));
+      MOE_CUDA_TRY(cudaEventElapsedTime(&ms, p.first, p.second));
+      sums[k] += ms;
+      ++counts[k];
+      ctx->ev_pool.push_back(p);
+    }
+    lists[k]->clear();
+  }
+  if (dispatch_ms) *dispatch_ms = sums[0];
+  if (n_dispatch) *n_dispatch = counts[0];
+  if (update_ms) *update_ms = sums[1];
+  if (n_update) *n_update = counts[1];
   return MOE_OK;
 }
 

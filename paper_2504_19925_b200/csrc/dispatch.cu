@@ -49,6 +49,7 @@ __global__ void __launch_bounds__(kThreads) k_hist(const __grid_constant__ HistA
   const int b = blockIdx.x % a.nb;   // tile
   const int tid = threadIdx.x, lane = tid & 31;
   const int32_t *ids = a.ids + (int64_t)v * a.npairs;
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // let k_scan get scheduled
   for (int e = tid; e < a.E; e += kThreads) hist[e] = 0;
   __syncthreads();
 
@@ -115,11 +116,19 @@ struct ScanArgs {
   int32_t *slot_load;    // [G*S]
   int32_t *send_count;   // [n_local][G*S]
   int64_t *counts_dev;   // [E]
+  int64_t *counts_host;  // [E] pinned host memory (UVA), nullable: C_e for the host planner
+  uint32_t *scan_done;   // block counter (self-resetting)
+  uint32_t *host_flag;   // pinned host word: set to `epoch` once counts_host is complete
   int32_t *err;
   int32_t fs[MOE_MAX_E + 1];
 };
 
 __device__ __forceinline__ int32_t ld_cg(const int32_t *p) { return __ldcg(p); }
+
+// Programmatic dependent launch (PDL): the dependent kernel may be scheduled before this one
+// ends; it must execute pdl_wait() before touching this kernel's outputs.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 __global__ void __launch_bounds__(kThreads) k_scan(const __grid_constant__ ScanArgs a) {
   const int e = blockIdx.x;
@@ -129,6 +138,8 @@ __global__ void __launch_bounds__(kThreads) k_scan(const __grid_constant__ ScanA
   __shared__ int32_t s_base, s_cnt, s_C, s_loc;
   __shared__ int32_t wsum[kThreads / 32];
   __shared__ int ok;
+  pdl_trigger();
+  pdl_wait();
 
   if (tid == 0) {
     ok = 1;
@@ -159,7 +170,10 @@ __global__ void __launch_bounds__(kThreads) k_scan(const __grid_constant__ ScanA
   const int32_t q = C / r, m = C % r;
   const int GS = a.G * a.S;
   if (v == 0) {
-    if (tid == 0) a.counts_dev[e] = C;
+    if (tid == 0) {
+      a.counts_dev[e] = C;
+      if (a.counts_host) a.counts_host[e] = C;  // straight to pinned host memory (PCIe write)
+    }
     for (int rho = tid; rho < r; rho += kThreads) a.slot_load[f0 + rho] = q + (rho < m ? 1 : 0);
   }
   for (int rho = tid; rho < r; rho += kThreads) {
@@ -191,6 +205,18 @@ __global__ void __launch_bounds__(kThreads) k_scan(const __grid_constant__ ScanA
     row[i] = run;
     run += c;
   }
+
+  // The last block publishes "C_t is on the host" (threadfence-reduction pattern): every
+  // block orders its host writes before its ticket; the last one releases the host flag.
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence_system();
+    if (atomicAdd(a.scan_done, 1u) == gridDim.x * gridDim.y - 1) {
+      *a.scan_done = 0;
+      __threadfence_system();
+      st_release_sys(a.host_flag, a.epoch);
+    }
+  }
 }
 
 struct ScatterArgs {
@@ -207,7 +233,7 @@ struct ScatterArgs {
 
 __global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ ScatterArgs a) {
   constexpr int kWarps = kThreads / 32;
-  constexpr int kRounds = kTilePairs / kThreads;  // 8 rounds of 32 consecutive pairs per warp
+  constexpr int kRounds = kTilePairs / kThreads;  // rounds of 32 consecutive pairs per warp
   __shared__ int32_t wcnt[kWarps][MOE_MAX_E];
   __shared__ ExpertInfo s_info[MOE_MAX_E];
   __shared__ int32_t s_blk[MOE_MAX_E];
@@ -215,6 +241,7 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ Sc
   const int b = blockIdx.x % a.nb;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t off_v = (int64_t)v * a.npairs;
+  pdl_wait();  // k_scan's outputs (einfo, scanned tile counts)
   for (int e = tid; e < a.E; e += kThreads) {
     s_info[e] = a.einfo[v * a.E + e];
     s_blk[e] = a.blk[((int64_t)v * a.E + e) * a.nb_max + b];
@@ -290,6 +317,25 @@ using namespace moe;
 
 int moe_validate_plan(const moe_ctx *ctx, const moe_plan_t *p, const char *what);  // ctx.cu
 
+namespace {
+// Launch with programmatic stream serialization (PDL): overlaps this kernel's launch with the
+// tail of the previous kernel in the stream; the kernel calls pdl_wait() before reading it.
+template <typename Args>
+cudaError_t launch_pdl(void (*kern)(Args), dim3 grid, cudaStream_t s, const Args &args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args);
+}
+}  // namespace
+
 extern "C" int moe_dispatch(moe_ctx *ctx, const int32_t *topk_ids, const float *gates, int64_t T,
                             const moe_plan_t *plan, const moe_dispatch_out *out, void *stream) {
   if (!ctx || !out) return fail(MOE_ERR_INVALID, "moe_dispatch: NULL ctx/out");
@@ -329,6 +375,7 @@ extern "C" int moe_dispatch(moe_ctx *ctx, const int32_t *topk_ids, const float *
   ha.done = ctx->done;
   ha.err = ctx->err;
   for (int h = 0; h < MOE_MAX_G; ++h) ha.dst[h] = real ? ctx->peer_sync[h] : ctx->sync;
+  const auto tev = timing_begin(ctx, s);
   k_hist<<<nb * ctx->n_local, kThreads, 0, s>>>(ha);
   MOE_CUDA_TRY(cudaGetLastError());
 
@@ -348,14 +395,20 @@ extern "C" int moe_dispatch(moe_ctx *ctx, const int32_t *topk_ids, const float *
   sa.slot_load = out->slot_load;
   sa.send_count = out->send_count;
   sa.counts_dev = out->counts_dev ? out->counts_dev : ctx->counts_dev;
+  sa.counts_host = nullptr;
+  if (out->counts_host) {  // C_t goes straight to pinned host memory (PAPER.md:709 fn: plan early)
+    void *dptr = nullptr;
+    if (cudaHostGetDevicePointer(&dptr, out->counts_host, 0) != cudaSuccess || !dptr) {
+      cudaGetLastError();
+      return fail(MOE_ERR_INVALID, "moe_dispatch: counts_host must be pinned (page-locked) host memory");
+    }
+    sa.counts_host = (int64_t *)dptr;
+  }
+  sa.scan_done = ctx->scan_done;
+  sa.host_flag = ctx->host_flag_dev;
   sa.err = ctx->err;
   for (int e = 0; e <= ctx->E; ++e) sa.fs[e] = plan->first_slot[e];
-  k_scan<<<dim3(ctx->E, ctx->n_local), kThreads, 0, s>>>(sa);
-  MOE_CUDA_TRY(cudaGetLastError());
-  if (out->counts_host)  // C_t to the host planner while the scatter runs (PAPER.md:709 fn)
-    MOE_CUDA_TRY(cudaMemcpyAsync(out->counts_host, sa.counts_dev, sizeof(int64_t) * ctx->E,
-                                 cudaMemcpyDeviceToHost, s));
-  MOE_CUDA_TRY(cudaEventRecord(ctx->counts_ev, s));
+  MOE_CUDA_TRY(launch_pdl(k_scan, dim3(ctx->E, ctx->n_local), s, sa));
   ctx->counts_pending = true;
 
   ScatterArgs ca{};
@@ -372,9 +425,7 @@ extern "C" int moe_dispatch(moe_ctx *ctx, const int32_t *topk_ids, const float *
   ca.send_pair = out->send_pair;
   ca.send_gate = out->send_gate;
   for (int e = 0; e <= ctx->E; ++e) ca.fs[e] = plan->first_slot[e];
-  if (npairs > 0) {
-    k_scatter<<<nb * ctx->n_local, kThreads, 0, s>>>(ca);
-    MOE_CUDA_TRY(cudaGetLastError());
-  }
+  if (npairs > 0) MOE_CUDA_TRY(launch_pdl(k_scatter, dim3(nb * ctx->n_local), s, ca));
+  timing_end(ctx->ev_disp, tev, s);
   return MOE_OK;
 }

@@ -14,7 +14,7 @@
 namespace moe {
 
 constexpr int kThreads = 256;          // block size of every hot kernel
-constexpr int kTilePairs = 2048;       // dispatch tile: 8 warps x 8 rounds x 32 lanes
+constexpr int kTilePairs = 512;        // dispatch tile: 8 warps x 2 rounds x 32 lanes
 constexpr int kVec = 8;                // elements per thread in the update (16 B of bf16)
 constexpr int kChunk = kThreads * kVec;  // update chunk: 2048 elements of one expert
 constexpr uint64_t kSpinTimeoutNs = 20ull * 1000 * 1000 * 1000;  // 20 s
@@ -77,11 +77,39 @@ struct moe_ctx {
   int32_t *err;             // device error bits
   unsigned long long *item_ctr;  // [2] dynamic-scheduling counters of k_update_tma (self-resetting)
   int64_t nb_max;
-  cudaEvent_t counts_ev;    // recorded after the C_e device->host copy
+  uint32_t *scan_done;      // k_scan block counter (self-resetting)
+  volatile uint32_t *host_flag;  // pinned host word: k_scan writes the dispatch epoch once C_e landed
+  uint32_t *host_flag_dev;       // its device (UVA) alias
   bool counts_pending;
 
   std::map<std::string, void *> opened;  // IPC handle bytes -> mapped base (dedup)
+
+  // measurement hooks (moe_ctx_set_timing): event pairs per stage, recycled
+  bool timing;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool, ev_disp, ev_upd;
 };
+
+namespace moe {
+// Record the start of a timed region (returns the pair to close), or {nullptr, nullptr}.
+inline std::pair<cudaEvent_t, cudaEvent_t> timing_begin(moe_ctx *c, cudaStream_t s) {
+  if (!c->timing) return {nullptr, nullptr};
+  std::pair<cudaEvent_t, cudaEvent_t> p{nullptr, nullptr};
+  if (!c->ev_pool.empty()) {
+    p = c->ev_pool.back();
+    c->ev_pool.pop_back();
+  } else if (cudaEventCreate(&p.first) != cudaSuccess || cudaEventCreate(&p.second) != cudaSuccess) {
+    return {nullptr, nullptr};
+  }
+  cudaEventRecord(p.first, s);
+  return p;
+}
+inline void timing_end(std::vector<std::pair<cudaEvent_t, cudaEvent_t>> &dst,
+                       std::pair<cudaEvent_t, cudaEvent_t> p, cudaStream_t s) {
+  if (!p.first) return;
+  cudaEventRecord(p.second, s);
+  dst.push_back(p);
+}
+}  // namespace moe
 
 namespace moe {
 

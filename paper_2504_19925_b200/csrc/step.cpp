@@ -1,0 +1,24 @@
+// moe_step: one whole iteration of the hot path, natively (no caller code between stages).
+//
+// Order (fig:design_diagram): dispatch with plan_t (a0 + a2), then the
+// placement scheduler on this iteration's popularity C_t (a1, for t+1; the paper notes step 6
+// "may execute earlier, even right after step 1", PAPER.md:709 fn), then reduce + Adam +
+// place (a3-a5).  The host planner runs while the device still executes the scatter kernel,
+// and the update is enqueued as soon as the plan exists.
+#include "common.h"
+
+extern "C" int moe_step(moe_ctx *ctx, const int32_t *topk_ids, const float *gates, int64_t T,
+                        const moe_plan_t *plan_cur, moe_plan_t *plan_next, int32_t policy,
+                        const moe_dispatch_out *out, const moe_adam_t *adam, void *stream) {
+  if (!ctx || !out || !plan_cur || !plan_next || !adam)
+    return moe::fail(MOE_ERR_INVALID, "moe_step: NULL argument");
+  if (!out->counts_host) return moe::fail(MOE_ERR_INVALID, "moe_step: out->counts_host is required");
+  int st = moe_dispatch(ctx, topk_ids, gates, T, plan_cur, out, stream);  // a0 + a2
+  if (st) return st;
+  st = moe_ctx_wait_counts(ctx);  // C_t on the host
+  if (st) return st;
+  st = moe_plan_ex(out->counts_host, plan_cur->E, plan_cur->G, plan_cur->S, policy, plan_next,
+                   nullptr);  // a1 -> plan_{t+1}
+  if (st) return st;
+  return moe_update(ctx, plan_cur, plan_next, adam, stream);  // a3 + a4 + a5
+}

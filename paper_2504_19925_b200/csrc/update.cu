@@ -584,14 +584,19 @@ int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *pl
   if (place_only || ctx->update_kernel == 0) {
     const int64_t grid = std::min<int64_t>(items, (int64_t)ctx->num_sms * ctx->upd_blocks_per_sm);
     if (grid > 0) {
+      const auto tev = place_only ? std::pair<cudaEvent_t, cudaEvent_t>{nullptr, nullptr}
+                                  : timing_begin(ctx, s);
       k_update<<<(unsigned)grid, kThreads, 0, s>>>(a);
       MOE_CUDA_TRY(cudaGetLastError());
+      timing_end(ctx->ev_upd, tev, s);
     }
   } else {
     const int64_t grid = std::min<int64_t>(items, (int64_t)ctx->num_sms * 2);
     if (grid > 0) {
+      const auto tev = timing_begin(ctx, s);
       k_update_tma<<<(unsigned)grid, kTmaThreads, kTmaSmem, s>>>(a);
       MOE_CUDA_TRY(cudaGetLastError());
+      timing_end(ctx->ev_upd, tev, s);
     }
   }
   if (multi) {  // barrier-out: every push into this GPU's slots has landed

@@ -80,12 +80,14 @@ class DecoupledExpertLayer:
         self.t += 1
 
     def iterate(self, topk_ids: torch.Tensor, gates: torch.Tensor, T: int, stream=None) -> api.Plan:
-        """The whole per-iteration hot path: dispatch -> plan -> reduce/Adam/place."""
+        """The whole per-iteration hot path in one native call (moe_step):
+        dispatch -> host plan (overlapping the scatter kernel) -> reduce/Adam/place."""
         if not self._connected:
             raise RuntimeError("real-mode layer: call connect() first")
-        self.dispatch(topk_ids, gates, T, stream)
-        nxt = self.plan_next()
-        self.update(nxt, stream)
+        nxt = api.moe_step(self.ctx, topk_ids, gates, T, self.plan, self.policy, self.out, self.adam,
+                           self.t, self.scale_mode, self.scale, stream)
+        self.plan = nxt
+        self.t += 1
         return nxt
 
     def close(self) -> None:

@@ -81,6 +81,40 @@ def test_edge_cases_empty_and_degenerate():
         run_parity("tiny-skew", 4, 1, trace=[(ids, gates)], T=ids.shape[0])
 
 
+def test_split_calls_equal_native_step_and_timing_hooks():
+    """moe_step (native a0..a5) == moe_dispatch + moe_ctx_wait_counts + moe_plan + moe_update,
+    bitwise; the timing hooks count one dispatch and one update launch per iteration."""
+    from paper_2504_19925_b200 import DecoupledExpertLayer
+    from paper_2504_19925_b200.api import synth_grads
+    wl = configs.CONFIGS["medium"]
+    G, S = 2, wl.S(2)
+    Tg = wl.T // G
+    a = DecoupledExpertLayer(wl.E, G, S, wl.k, wl.P, Tg, rank=-1, device=0, seed=5)
+    b = DecoupledExpertLayer(wl.E, G, S, wl.k, wl.P, Tg, rank=-1, device=0, seed=5)
+    a.ctx.set_timing(True)
+    tr = traces.make_trace(wl, iters=4)
+    for t, (ids, gates) in enumerate(tr):
+        for L in (a, b):
+            for v in range(G):
+                synth_grads(L.slot_g[v], 5, t, v * S, S, wl.P)
+        ids_d, gates_d = torch.from_numpy(ids).cuda(), torch.from_numpy(gates).cuda()
+        a.iterate(ids_d, gates_d, Tg)
+        b.dispatch(ids_d, gates_d, Tg)
+        nxt = b.plan_next()
+        b.update(nxt)
+        assert a.plan.first_slot.tolist() == b.plan.first_slot.tolist()
+    torch.cuda.synchronize()
+    for v in range(G):
+        assert torch.equal(a.master[v], b.master[v]) and torch.equal(a.adam_v[v], b.adam_v[v])
+        assert torch.equal(a.slot_w[v].view(torch.int16), b.slot_w[v].view(torch.int16))
+    tm = a.ctx.get_timing()
+    assert tm["n_dispatch"] == 4 and tm["n_update"] == 4
+    assert tm["dispatch_ms"] > 0 and tm["update_ms"] > 0
+    assert a.ctx.get_timing()["n_update"] == 0
+    a.close()
+    b.close()
+
+
 def test_invalid_ids_raise_data_error():
     from paper_2504_19925_b200 import DecoupledExpertLayer, MoeError
     layer = DecoupledExpertLayer(8, 1, 8, 2, 4096, 128, rank=0, device=0)
