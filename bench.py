@@ -285,6 +285,12 @@ def gpu_arm(args, wl):
 
     peak_hbm, peak_src, _ = _peaks()
     ab = algorithmic_bytes(wl, G, S)
+    if args.traffic is None:  # DRAM bytes per launch from the committed ncu --set full capture
+        try:
+            tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+            args.traffic = tj.get(f"{wl.name}/G={G}/k_update_tma", {}).get("dram_bytes")
+        except Exception:
+            args.traffic = None
     if G == 1:
         achieved = ab["update_hbm"] / (upd_avg * 1e-3) / 1e9
         roof = {"kernel": "k_update (fused reduce+Adam+place)", "bound": "hbm",
