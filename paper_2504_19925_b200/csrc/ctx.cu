@@ -161,7 +161,7 @@ extern "C" int moe_ctx_create(const moe_ctx_desc *d, moe_ctx **out) {
   chk(cudaMalloc(&c->einfo, sizeof(ExpertInfo) * n_local * c->E));
   chk(cudaMalloc(&c->counts_dev, sizeof(int64_t) * c->E));
   chk(cudaMalloc(&c->err, sizeof(int32_t)));
-  chk(cudaMalloc(&c->item_ctr, 2 * sizeof(unsigned long long)));
+  chk(cudaMalloc(&c->item_ctr, 3 * sizeof(unsigned long long)));
   chk(cudaMalloc(&c->scan_done, sizeof(uint32_t)));
   {
     void *hf = nullptr;
@@ -179,7 +179,7 @@ extern "C" int moe_ctx_create(const moe_ctx_desc *d, moe_ctx **out) {
     chk(cudaMemset(c->cnt_local, 0, sizeof(int32_t) * n_local * c->E));
     chk(cudaMemset(c->done, 0, sizeof(uint32_t) * n_local));
     chk(cudaMemset(c->err, 0, sizeof(int32_t)));
-    chk(cudaMemset(c->item_ctr, 0, 2 * sizeof(unsigned long long)));
+    chk(cudaMemset(c->item_ctr, 0, 3 * sizeof(unsigned long long)));
     chk(cudaMemset(c->scan_done, 0, sizeof(uint32_t)));
     chk(cudaDeviceSynchronize());
   }

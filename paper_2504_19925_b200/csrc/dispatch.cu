@@ -32,7 +32,7 @@ namespace {
 struct HistArgs {
   const int32_t *ids;
   int64_t npairs;  // pairs per rank = T*k
-  int32_t k, E, G, rank, real, nb, nb_max;
+  int32_t k, E, G, rank, real, nb, nb_max, tile;
   uint32_t epoch;
   int32_t parity;
   int32_t *blk;        // [n_local][E][nb_max]
@@ -53,9 +53,9 @@ __global__ void __launch_bounds__(kThreads) k_hist(const __grid_constant__ HistA
   for (int e = tid; e < a.E; e += kThreads) hist[e] = 0;
   __syncthreads();
 
-  const int64_t t0 = (int64_t)b * kTilePairs;
+  const int64_t t0 = (int64_t)b * a.tile;
 #pragma unroll 4
-  for (int i = 0; i < kTilePairs / kThreads; ++i) {
+  for (int i = 0; i < a.tile / kThreads; ++i) {
     const int64_t p = t0 + i * kThreads + tid;
     const bool in = p < a.npairs;
     int e = in ? __ldg(ids + p) : -1;
@@ -149,20 +149,23 @@ __global__ void __launch_bounds__(kThreads) k_scan(const __grid_constant__ ScanA
   }
   __syncthreads();
   if (!ok) return;
-  if (tid == 0) {
+  if (warp == 0) {  // warp-parallel: C_e and this rank's base (over GPUs), loc_off (over experts)
     const int32_t(*x)[MOE_MAX_E] = a.sync->xcnt[a.parity];
-    int32_t C = 0, base = 0;
-    for (int h = 0; h < a.G; ++h) {
-      const int32_t c = ld_cg(&x[h][e]);
-      if (h < grank) base += c;
-      C += c;
+    const int32_t c = lane < a.G ? ld_cg(&x[lane][e]) : 0;
+    int32_t C = c, base = lane < grank ? c : 0, loc = 0;
+    for (int e2 = lane; e2 < e; e2 += 32) loc += ld_cg(&x[grank][e2]);
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      C += __shfl_xor_sync(0xffffffffu, C, d);
+      base += __shfl_xor_sync(0xffffffffu, base, d);
+      loc += __shfl_xor_sync(0xffffffffu, loc, d);
     }
-    int32_t loc = 0;
-    for (int e2 = 0; e2 < e; ++e2) loc += ld_cg(&x[grank][e2]);
-    s_base = base;
-    s_cnt = ld_cg(&x[grank][e]);
-    s_C = C;
-    s_loc = loc;
+    if (lane == 0) {
+      s_base = base;
+      s_cnt = ld_cg(&x[grank][e]);
+      s_C = C;
+      s_loc = loc;
+    }
   }
   __syncthreads();
   const int32_t C = s_C, base = s_base, cnt = s_cnt;
@@ -223,7 +226,7 @@ struct ScatterArgs {
   const int32_t *ids;
   const float *gates;
   int64_t npairs;
-  int32_t E, nb, nb_max;
+  int32_t E, nb, nb_max, tile;
   const int32_t *blk;
   const ExpertInfo *einfo;
   int32_t *dest_slot, *dest_off, *send_pair;
@@ -233,14 +236,22 @@ struct ScatterArgs {
 
 __global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ ScatterArgs a) {
   constexpr int kWarps = kThreads / 32;
-  constexpr int kRounds = kTilePairs / kThreads;  // rounds of 32 consecutive pairs per warp
   __shared__ int32_t wcnt[kWarps][MOE_MAX_E];
   __shared__ ExpertInfo s_info[MOE_MAX_E];
   __shared__ int32_t s_blk[MOE_MAX_E];
+  extern __shared__ int32_t s_tile[];  // [tile] ids, then [tile] gates (bit patterns)
   const int v = blockIdx.x / a.nb;
   const int b = blockIdx.x % a.nb;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t off_v = (int64_t)v * a.npairs;
+  {  // stage the tile's ids and gates (inputs, not produced by k_scan): independent, coalesced
+    const int64_t t0 = (int64_t)b * a.tile;
+    const int n = (int)(a.npairs - t0 < a.tile ? a.npairs - t0 : a.tile);
+    for (int i = tid; i < n; i += kThreads) {
+      s_tile[i] = __ldg(a.ids + off_v + t0 + i);
+      s_tile[a.tile + i] = __float_as_int(__ldg(a.gates + off_v + t0 + i));
+    }
+  }
   pdl_wait();  // k_scan's outputs (einfo, scanned tile counts)
   for (int e = tid; e < a.E; e += kThreads) {
     s_info[e] = a.einfo[v * a.E + e];
@@ -250,29 +261,26 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ Sc
   }
   __syncthreads();
 
-  // warp w owns the 256 consecutive pairs [w*256, (w+1)*256) of the tile, in 8 rounds of 32:
-  // pair order == (warp, round, lane) order, so ranks below are stable.
-  const int64_t seg = (int64_t)b * kTilePairs + warp * (kRounds * 32);
-  int32_t er[kRounds], rk[kRounds];
+  // Warp w owns the consecutive pairs [w*R*32, (w+1)*R*32) of the tile (R = tile/256 rounds of
+  // 32): pair order == (warp, round, lane) order, so the ranks below are stable.
+  // Pass 1 counts each warp's pairs per expert; an exclusive prefix over warps turns the
+  // counts into starting ranks; pass 2 re-walks the segment, ranking each pair as
+  // start + (lower lanes of the round with the same expert) and advancing the start.
+  const int rounds = a.tile / kThreads;
+  const int64_t seg = (int64_t)b * a.tile + (int64_t)warp * rounds * 32;
   const unsigned lt = (1u << lane) - 1u;
-#pragma unroll
-  for (int r = 0; r < kRounds; ++r) {
+  const int64_t tbase = (int64_t)b * a.tile;
+  for (int r = 0; r < rounds; ++r) {  // pass 1
     const int64_t p = seg + r * 32 + lane;
     const bool in = p < a.npairs;
-    const int e = in ? __ldg(a.ids + off_v + p) : -1;
+    const int e = in ? s_tile[p - tbase] : -1;
     const bool valid = in && (unsigned)e < (unsigned)a.E;
     const unsigned act = __ballot_sync(0xffffffffu, valid);
-    unsigned peers = 0;
-    int myr = 0;
     if (valid) {
-      peers = __match_any_sync(act, e);
-      myr = wcnt[warp][e] + __popc(peers & lt);
+      const unsigned peers = __match_any_sync(act, e);
+      if (lane == __ffs(peers) - 1) wcnt[warp][e] += __popc(peers);
     }
     __syncwarp();
-    if (valid && lane == __ffs(peers) - 1) wcnt[warp][e] += __popc(peers);
-    __syncwarp();
-    er[r] = in ? (valid ? e : -2) : -1;
-    rk[r] = myr;
   }
   __syncthreads();
   for (int e = tid; e < a.E; e += kThreads) {  // exclusive prefix over warps, per expert
@@ -285,28 +293,39 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ Sc
     }
   }
   __syncthreads();
-#pragma unroll
-  for (int r = 0; r < kRounds; ++r) {
+  for (int r = 0; r < rounds; ++r) {  // pass 2
     const int64_t p = seg + r * 32 + lane;
-    const int e = er[r];
-    if (e == -1) continue;
-    if (e < 0) {  // invalid id: flagged by k_hist; keep memory safe
+    const bool in = p < a.npairs;
+    const int e = in ? s_tile[p - tbase] : -1;
+    const bool valid = in && (unsigned)e < (unsigned)a.E;
+    const unsigned act = __ballot_sync(0xffffffffu, valid);
+    unsigned peers = 0;
+    int32_t wr = 0;
+    if (valid) {
+      peers = __match_any_sync(act, e);
+      wr = wcnt[warp][e] + __popc(peers & lt);
+    }
+    __syncwarp();
+    if (valid && lane == __ffs(peers) - 1) wcnt[warp][e] += __popc(peers);
+    __syncwarp();
+    if (!in) continue;
+    if (!valid) {  // invalid id: flagged by k_hist; keep memory safe
       a.dest_slot[off_v + p] = -1;
       a.dest_off[off_v + p] = -1;
       continue;
     }
-    const ExpertInfo in = s_info[e];
-    const int32_t lr = s_blk[e] + wcnt[warp][e] + rk[r];  // rank within this rank's pairs of e
-    const int32_t R = in.base + lr;                         // global rank within expert e
-    const int32_t q = in.q, m = in.m;
+    const ExpertInfo info = s_info[e];
+    const int32_t lr = s_blk[e] + wr;  // rank within this rank's pairs of e
+    const int32_t R = info.base + lr;  // global rank within expert e
+    const int32_t q = info.q, m = info.m;
     const int32_t big = m * (q + 1);
     const int32_t rho = R < big ? R / (q + 1) : m + (R - big) / q;
     const int32_t off = R - (rho * q + min(rho, m));
     a.dest_slot[off_v + p] = a.fs[e] + rho;
     a.dest_off[off_v + p] = off;
-    const int64_t pos = off_v + in.loc_off + lr;
+    const int64_t pos = off_v + info.loc_off + lr;
     a.send_pair[pos] = (int32_t)p;
-    a.send_gate[pos] = __ldg(a.gates + off_v + p);
+    a.send_gate[pos] = __int_as_float(s_tile[a.tile + (p - tbase)]);
   }
 }
 
@@ -321,11 +340,12 @@ namespace {
 // Launch with programmatic stream serialization (PDL): overlaps this kernel's launch with the
 // tail of the previous kernel in the stream; the kernel calls pdl_wait() before reading it.
 template <typename Args>
-cudaError_t launch_pdl(void (*kern)(Args), dim3 grid, cudaStream_t s, const Args &args) {
+cudaError_t launch_pdl(void (*kern)(Args), dim3 grid, cudaStream_t s, const Args &args,
+                       size_t smem = 0) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -353,7 +373,14 @@ extern "C" int moe_dispatch(moe_ctx *ctx, const int32_t *topk_ids, const float *
   MOE_CUDA_TRY(cudaSetDevice(ctx->device));
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t npairs = T * ctx->k;
-  const int nb = (int)std::max<int64_t>(1, (npairs + kTilePairs - 1) / kTilePairs);
+  // Tile size: >= kTilePairs, grown (in multiples of the block size) so that all local ranks
+  // together launch about 4 tiles per SM: large inputs get long tiles (few per-tile counts,
+  // little atomic traffic), small inputs still fill the GPU.
+  const int64_t per_rank_tiles = std::max<int64_t>(1, (int64_t)4 * ctx->num_sms / ctx->n_local);
+  int64_t tile = (npairs + per_rank_tiles - 1) / per_rank_tiles;
+  tile = std::max<int64_t>(kTilePairs, (tile + kThreads - 1) / kThreads * kThreads);
+  tile = std::min<int64_t>(tile, kMaxTilePairs);  // k_scatter stages ids + gates in smem
+  const int nb = (int)std::max<int64_t>(1, (npairs + tile - 1) / tile);
   const uint32_t epoch = ++ctx->disp_epoch;
   const int parity = (int)(epoch & 1u);
   const int real = ctx->rank >= 0 ? 1 : 0;
@@ -367,6 +394,7 @@ extern "C" int moe_dispatch(moe_ctx *ctx, const int32_t *topk_ids, const float *
   ha.rank = ctx->rank;
   ha.real = real;
   ha.nb = nb;
+  ha.tile = (int)tile;
   ha.nb_max = (int)ctx->nb_max;
   ha.epoch = epoch;
   ha.parity = parity;
@@ -417,6 +445,7 @@ extern "C" int moe_dispatch(moe_ctx *ctx, const int32_t *topk_ids, const float *
   ca.npairs = npairs;
   ca.E = ctx->E;
   ca.nb = nb;
+  ca.tile = (int)tile;
   ca.nb_max = (int)ctx->nb_max;
   ca.blk = ctx->blk;
   ca.einfo = ctx->einfo;
@@ -425,7 +454,8 @@ extern "C" int moe_dispatch(moe_ctx *ctx, const int32_t *topk_ids, const float *
   ca.send_pair = out->send_pair;
   ca.send_gate = out->send_gate;
   for (int e = 0; e <= ctx->E; ++e) ca.fs[e] = plan->first_slot[e];
-  if (npairs > 0) MOE_CUDA_TRY(launch_pdl(k_scatter, dim3(nb * ctx->n_local), s, ca));
+  if (npairs > 0)
+    MOE_CUDA_TRY(launch_pdl(k_scatter, dim3(nb * ctx->n_local), s, ca, (size_t)2 * tile * sizeof(int32_t)));
   timing_end(ctx->ev_disp, tev, s);
   return MOE_OK;
 }

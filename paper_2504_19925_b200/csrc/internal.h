@@ -14,7 +14,8 @@
 namespace moe {
 
 constexpr int kThreads = 256;          // block size of every hot kernel
-constexpr int kTilePairs = 512;        // dispatch tile: 8 warps x 2 rounds x 32 lanes
+constexpr int kTilePairs = 512;        // minimum dispatch tile: 8 warps x 2 rounds x 32 lanes
+constexpr int kMaxTilePairs = 4096;    // maximum (k_scatter stages 8 B/pair in shared memory)
 constexpr int kVec = 8;                // elements per thread in the update (16 B of bf16)
 constexpr int kChunk = kThreads * kVec;  // update chunk: 2048 elements of one expert
 constexpr uint64_t kSpinTimeoutNs = 20ull * 1000 * 1000 * 1000;  // 20 s
@@ -75,7 +76,7 @@ struct moe_ctx {
   moe::ExpertInfo *einfo;   // [n_local][E]
   int64_t *counts_dev;      // [E]
   int32_t *err;             // device error bits
-  unsigned long long *item_ctr;  // [2] dynamic-scheduling counters of k_update_tma (self-resetting)
+  unsigned long long *item_ctr;  // [3] counters of k_update_tma (self-resetting)
   int64_t nb_max;
   uint32_t *scan_done;      // k_scan block counter (self-resetting)
   volatile uint32_t *host_flag;  // pinned host word: k_scan writes the dispatch epoch once C_e landed

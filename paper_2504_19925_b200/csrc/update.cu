@@ -44,7 +44,14 @@ struct UpdArgs {
   float *master[MOE_MAX_G];          // fp32 [E][Pg], per owner
   float *mom1[MOE_MAX_G];
   float *mom2[MOE_MAX_G];
-  unsigned long long *item_ctr;  // [2] k_update_tma work counter + finished-CTA counter (zero between launches)
+  unsigned long long *item_ctr;  // [3] k_update_tma: work counter, producers done, CTAs done
+                                 //     (all zero between launches; the last finisher resets)
+  // in-kernel cross-GPU barriers of k_update_tma (real mode, G > 1)
+  int32_t fused_barrier, rank;
+  uint32_t epoch;
+  int32_t *err;
+  SyncBuf *sync_local;
+  SyncBuf *sync_peer[MOE_MAX_G];
 };
 
 __device__ __forceinline__ uint4 ld_stream(const uint16_t *p) {
@@ -311,8 +318,19 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_update_tma(const __grid_cons
   const int64_t total = per_owner * a.o_count;
   const int64_t P = a.P;
 
+  // Barrier-in (real mode): "every GPU's slot grads are ready".  This GPU's earlier stream
+  // work (the backward that wrote its grads) is complete when this kernel starts; one thread
+  // tells every peer so, and each producer waits for all GPUs before its first (peer) copy.
+  // The consumers only touch peer memory after receiving an item from their producer.
+  if (a.fused_barrier && blockIdx.x == 0 && threadIdx.x == 0) {
+    __threadfence_system();
+    for (int h = 0; h < a.G; ++h) st_release_sys(&a.sync_peer[h]->upd_in[a.rank], a.epoch);
+  }
+
   if (warp == kConsumerWarps) {  // ---------------- producer ----------------
     if (lane != 0) return;
+    if (a.fused_barrier)
+      for (int h = 0; h < a.G; ++h) wait_flag(&a.sync_local->upd_in[h], a.epoch, a.err);
     uint32_t si = 0, gi_ = 0;
     for (;;) {
       // dynamic scheduling: claim the next item (chunk-major order, see kItemOrder note)
@@ -457,6 +475,21 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_update_tma(const __grid_cons
     pv[1] = make_float4(v[4], v[5], v[6], v[7]);
     place_to(a, e, (int64_t)o * a.Pg + loc, wb);                          // a5
   }
+
+  // Barrier-out (real mode): "every push into every GPU's slots has landed".  Each consumer
+  // fences its own (peer) stores at system scope; the consumer warps meet on a named barrier;
+  // the last CTA of this GPU signals every peer and waits for all of them, so this kernel ends
+  // only after all weights of plan_next are in place on this GPU.
+  if (a.fused_barrier) {
+    __threadfence_system();
+    asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory");
+    if (tid == 0 && atomicAdd(a.item_ctr + 2, 1ull) == gridDim.x - 1) {
+      a.item_ctr[2] = 0;
+      __threadfence_system();
+      for (int h = 0; h < a.G; ++h) st_release_sys(&a.sync_peer[h]->upd_out[a.rank], a.epoch);
+      for (int h = 0; h < a.G; ++h) wait_flag(&a.sync_local->upd_out[h], a.epoch, a.err);
+    }
+  }
 }
 
 // Cross-GPU barrier: signal every peer (release, system scope), then wait for every peer.
@@ -568,8 +601,15 @@ int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *pl
   a.item_ctr = ctx->item_ctr;
   const bool multi = ctx->rank >= 0 && ctx->G > 1;
   const uint32_t epoch = ++ctx->upd_epoch;
+  const bool tma = !place_only && ctx->update_kernel != 0;
+  a.fused_barrier = (multi && tma) ? 1 : 0;  // k_update_tma carries both barriers itself
+  a.rank = ctx->rank;
+  a.epoch = epoch;
+  a.err = ctx->err;
+  a.sync_local = ctx->sync;
+  for (int h = 0; h < ctx->G; ++h) a.sync_peer[h] = ctx->peer_sync[h];
   BarrierArgs ba{};
-  if (multi) {  // barrier-in: every GPU's grads are ready before any pull
+  if (multi && !tma) {  // barrier-in: every GPU's grads are ready before any pull
     ba.local = ctx->sync;
     for (int h = 0; h < ctx->G; ++h) ba.peer[h] = ctx->peer_sync[h];
     ba.G = ctx->G;
@@ -599,7 +639,7 @@ int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *pl
       timing_end(ctx->ev_upd, tev, s);
     }
   }
-  if (multi) {  // barrier-out: every push into this GPU's slots has landed
+  if (multi && !tma) {  // barrier-out: every push into this GPU's slots has landed
     ba.which = 1;
     k_barrier<<<1, 32, 0, s>>>(ba);
     MOE_CUDA_TRY(cudaGetLastError());
