@@ -92,14 +92,48 @@ class ClockSampler:
                 "reasons": sorted(reasons)}
 
 
-def algorithmic_bytes(wl, G: int, S: int) -> dict:
-    """per GPU per iteration."""
-    P, E = wl.P, wl.E
+def update_stage_bytes(fs_cur, fs_next, G: int, S: int, P: int, E: int, dedup: bool):
+    """Algorithmic bytes of one update stage, from the two plans.
+
+    Returns (max over GPUs of HBM bytes, max over GPUs and directions of NVLink bytes).
+    Plain path: owner g reads its Pg slice of every replica of e from the GPU holding it and
+    writes its bf16 slice into every next-plan slot of e; GPU g also reads+writes its
+    master/m/v (24 B/element).  At G = 1 this is 2*S*P + 24*E*P + 2*S*P, and the NVLink bytes
+    per direction are 4*S*(G-1)/G*P for ANY placement (App. E).
+    De-dup (row f1): a GPU with r >= 3 replicas of e first reads them (2rP) and writes an fp32
+    partial (4P) that owners then read (4 B/element); a remote GPU receives each shard once
+    and copies it into its other slots of e (read + write of the remote owners' ranges).
+    """
     Pg = P // G
-    pairs = (wl.T // G) * wl.k
-    upd_hbm = 2 * S * P + 24 * E * Pg + 2 * S * P       # grads read + master/m/v rw + weights written
-    nvl_dir = 2 * (2 * S * (G - 1) * P // G)             # reduce pulls + place pushes, per direction
-    return {"dispatch_hbm": 28 * pairs, "update_hbm": upd_hbm, "update_nvlink_per_dir": nvl_dir}
+    hbm = [24 * E * Pg] * G
+    nin, nout = [0] * G, [0] * G
+    for e in range(E):
+        for h in range(G):
+            r = min(int(fs_cur[e + 1]), (h + 1) * S) - max(int(fs_cur[e]), h * S)
+            if r <= 0:
+                continue
+            partial = dedup and r >= 3
+            if partial:
+                hbm[h] += 2 * r * P + 4 * P
+            per_owner = 4 * Pg if partial else 2 * r * Pg
+            for g in range(G):
+                hbm[h] += per_owner
+                if g != h:
+                    nout[h] += per_owner
+                    nin[g] += per_owner
+        for h in range(G):
+            r = min(int(fs_next[e + 1]), (h + 1) * S) - max(int(fs_next[e]), h * S)
+            if r <= 0:
+                continue
+            for g in range(G):
+                n = r if (not dedup or g == h) else 1
+                hbm[h] += 2 * Pg * n
+                if g != h:
+                    nout[g] += 2 * Pg * n
+                    nin[h] += 2 * Pg * n
+            if dedup and r > 1:
+                hbm[h] += (r - 1) * 2 * 2 * (P - Pg)
+    return max(hbm), max(max(nin), max(nout))
 
 
 # ------------------------------------------------------------------------------------------
@@ -199,7 +233,7 @@ def gpu_arm(args, wl):
     Tg = wl.tokens_per_rank(G)
     seed = configs.seed_for(wl.name)
     layer = DecoupledExpertLayer(wl.E, G, S, wl.k, wl.P, Tg, rank=rank if G > 1 else 0,
-                                 device=local, seed=seed)
+                                 device=local, seed=seed, dedup=args.dedup)
     if G > 1:
         layer.connect()
     n_tr = min(args.warmup + args.steps, args.trace_iters)
@@ -216,9 +250,14 @@ def gpu_arm(args, wl):
 
     stream = torch.cuda.current_stream()
 
-    def step(i):
+    plans = []  # (first_slot of plan_t, of plan_t+1) per timed step, for the byte accounting
+
+    def step(i, record=False):
         t = i % n_tr
-        layer.iterate(ids_d[t], gates_d[t], Tg)    # moe_step: a0+a2 -> a1 (host) -> a3+a4+a5
+        cur = layer.plan.first_slot.copy() if record else None
+        nxt = layer.iterate(ids_d[t], gates_d[t], Tg)  # moe_step: a0+a2 -> a1 (host) -> a3+a4+a5
+        if record:
+            plans.append((cur, nxt.first_slot.copy()))
 
     for i in range(args.warmup):
         step(i)
@@ -235,7 +274,7 @@ def gpu_arm(args, wl):
     start.record(stream)
     h0 = time.perf_counter()
     for i in range(K):
-        step(args.warmup + i)
+        step(args.warmup + i, record=True)
     h1 = time.perf_counter()
     end.record(stream)
     barrier()
@@ -246,10 +285,13 @@ def gpu_arm(args, wl):
     total_ms = start.elapsed_time(end)
     upd_avg_local = tm["update_ms"] / max(1, tm["n_update"])
     disp_avg_local = tm["dispatch_ms"] / max(1, tm["n_dispatch"])
-    t = torch.tensor([total_ms, upd_avg_local, disp_avg_local], device="cuda")
+    pre_avg_local = tm["presum_ms"] / K
+    rep_avg_local = tm["replicate_ms"] / K
+    t = torch.tensor([total_ms, upd_avg_local, disp_avg_local, pre_avg_local, rep_avg_local],
+                     device="cuda")
     if G > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms, upd_avg, disp_avg = (float(x) for x in t.tolist())
+    total_ms, upd_avg, disp_avg, pre_avg, rep_avg = (float(x) for x in t.tolist())
     host_ms = 1e3 * (h1 - h0) / K
     ms_iter = total_ms / K
 
@@ -284,40 +326,42 @@ def gpu_arm(args, wl):
         layer.ctx.check()
 
     peak_hbm, peak_src, _ = _peaks()
-    ab = algorithmic_bytes(wl, G, S)
     if args.traffic is None:  # DRAM bytes per launch from the committed ncu --set full capture
         try:
             tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
             args.traffic = tj.get(f"{wl.name}/G={G}/k_update_tma", {}).get("dram_bytes")
         except Exception:
             args.traffic = None
-    if G == 1:
-        achieved = ab["update_hbm"] / (upd_avg * 1e-3) / 1e9
-        roof = {"kernel": "k_update (fused reduce+Adam+place)", "bound": "hbm",
-                "achieved": round(achieved, 1), "peak": peak_hbm, "unit": "GB/s",
-                "frac": round(achieved / peak_hbm, 4), "traffic": args.traffic,
-                "algorithmic_bytes_per_launch": ab["update_hbm"], "peak_source": peak_src,
+    # algorithmic bytes of the update stage, per timed iteration from the actual plans
+    hbm_b, nvl_b = [], []
+    for fc, fn in plans:
+        hb, nb = update_stage_bytes(fc, fn, G, S, wl.P, wl.E, args.dedup)
+        hbm_b.append(hb)
+        nvl_b.append(nb)
+    upd_hbm = statistics.mean(hbm_b)
+    upd_nvl = statistics.mean(nvl_b)
+    t_hbm = upd_hbm / (peak_hbm * 1e9)
+    t_nvl = upd_nvl / (GUIDE_NVLINK_GBS * 1e9) if G > 1 else 0.0
+    kname = ("update stage (k_presum + k_update_tma + k_replicate)" if args.dedup
+             else "k_update_tma (fused reduce+Adam+place)")
+    if t_nvl > t_hbm:
+        achieved = upd_nvl / (upd_avg * 1e-3) / 1e9
+        roof = {"kernel": kname + ", NVLink pulls/pushes", "bound": "nvlink",
+                "achieved": round(achieved, 1), "peak": GUIDE_NVLINK_GBS, "unit": "GB/s",
+                "frac": round(achieved / GUIDE_NVLINK_GBS, 4), "traffic": None,
+                "algorithmic_bytes_per_launch": int(upd_nvl),
+                "peak_source": "B200_PROFILING.md measured peer copy per direction (900 nominal)",
                 "avg_launch_ms": round(upd_avg, 4)}
     else:
-        t_hbm = ab["update_hbm"] / (peak_hbm * 1e9)
-        t_nvl = ab["update_nvlink_per_dir"] / (GUIDE_NVLINK_GBS * 1e9)
-        if t_nvl >= t_hbm:
-            achieved = ab["update_nvlink_per_dir"] / (upd_avg * 1e-3) / 1e9
-            roof = {"kernel": "k_update (fused reduce+Adam+place, NVLink pulls/pushes)",
-                    "bound": "nvlink", "achieved": round(achieved, 1), "peak": GUIDE_NVLINK_GBS,
-                    "unit": "GB/s", "frac": round(achieved / GUIDE_NVLINK_GBS, 4), "traffic": None,
-                    "algorithmic_bytes_per_launch": ab["update_nvlink_per_dir"],
-                    "peak_source": "B200_PROFILING.md measured peer copy per direction (900 nominal)",
-                    "avg_launch_ms": round(upd_avg, 4)}
-        else:
-            achieved = ab["update_hbm"] / (upd_avg * 1e-3) / 1e9
-            roof = {"kernel": "k_update", "bound": "hbm", "achieved": round(achieved, 1),
-                    "peak": peak_hbm, "unit": "GB/s", "frac": round(achieved / peak_hbm, 4),
-                    "traffic": None, "algorithmic_bytes_per_launch": ab["update_hbm"],
-                    "peak_source": peak_src, "avg_launch_ms": round(upd_avg, 4)}
-    t_roof_step = max((ab["update_hbm"] + ab["dispatch_hbm"]) / (peak_hbm * 1e9),
-                      ab["update_nvlink_per_dir"] / (GUIDE_NVLINK_GBS * 1e9) if G > 1 else 0.0)
-    launches_per_step = 3 + 1 + (2 if G > 1 else 0)
+        achieved = upd_hbm / (upd_avg * 1e-3) / 1e9
+        roof = {"kernel": kname, "bound": "hbm", "achieved": round(achieved, 1), "peak": peak_hbm,
+                "unit": "GB/s", "frac": round(achieved / peak_hbm, 4),
+                "traffic": args.traffic if (G == 1 and not args.dedup) else None,
+                "algorithmic_bytes_per_launch": int(upd_hbm), "peak_source": peak_src,
+                "avg_launch_ms": round(upd_avg, 4)}
+    disp_hbm = 28 * (wl.T // G) * wl.k
+    t_roof_step = max((upd_hbm + disp_hbm) / (peak_hbm * 1e9), t_nvl)
+    launches_per_step = 3 + 1 + (2 if args.dedup else 0)
 
     cpu = None
     if rank == 0 and G == 1 and not args.no_cpu_baseline:
@@ -330,15 +374,17 @@ def gpu_arm(args, wl):
             "steps": K, "warmup": args.warmup, "ms_per_step": round(ms_iter, 4),
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (walk-spike routing trace, counter-hash grads)",
-            "config": _config(wl, G),
+            "config": dict(_config(wl, G), dedup=bool(args.dedup)),
             "roofline": roof,
             "step_roofline": {"t_roof_ms": round(t_roof_step * 1e3, 4),
                               "frac": round(t_roof_step * 1e3 / ms_iter, 4),
                               "basis": "max(HBM bytes of dispatch+update / peak HBM, NVLink bytes/dir / 770 GB/s)"},
-            "stages_ms": {"dispatch": round(disp_avg, 4), "update_kernel": round(upd_avg, 4),
+            "stages_ms": {"dispatch": round(disp_avg, 4), "update_stage": round(upd_avg, 4),
+                          "presum": round(pre_avg, 4), "replicate": round(rep_avg, 4),
                           "host_enqueue_per_step": round(host_ms, 4),
-                          "note": "library CUDA events (moe_ctx_set_timing) around the 3 dispatch "
-                                  "kernels and around the update kernel (barriers excluded)"},
+                          "note": "library CUDA events (moe_ctx_set_timing) on the launching stream: "
+                                  "the 3 dispatch kernels; the update stage (= k_update_tma, or with "
+                                  "de-dup k_presum + k_update_tma + k_replicate); max over ranks"},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * K,
             "clocks": clocks,
         }
@@ -359,6 +405,8 @@ def main():
     ap.add_argument("--trace-iters", type=int, default=25)
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dedup", action="store_true",
+                    help="locality de-duplication (MOE_OPT_DEDUP, SURVEY row f1); G > 1 only")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-iters", type=int, default=3)
     ap.add_argument("--cpu-frac", type=int, default=64)
@@ -367,6 +415,8 @@ def main():
                     help="dram bytes per k_update launch from an ncu --set full capture")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
+    if args.gpus == 1:
+        args.dedup = False  # nothing crosses NVLink at G = 1; the library ignores it too
     from synth import configs
     wl = configs.CONFIGS[args.config]
     if args.impl == "reference":

@@ -50,7 +50,7 @@
 extern "C" {
 #endif
 
-#define MOE_ABI_VERSION 1
+#define MOE_ABI_VERSION 2
 #define MOE_MAX_E 256     /* experts per layer                              */
 #define MOE_MAX_G 8       /* GPUs: one NVSwitch box                         */
 #define MOE_MAX_SLOTS 4096 /* G*S                                           */
@@ -127,7 +127,19 @@ typedef struct {
   float *const *master;  /* fp32 [E][Pg]  owner shard: master weights                    */
   float *const *adam_m;  /* fp32 [E][Pg]  owner shard: first moment                      */
   float *const *adam_v;  /* fp32 [E][Pg]  owner shard: second moment                     */
+  int32_t options;       /* bit mask of MOE_OPT_*                                          */
 } moe_ctx_desc;
+
+/* Locality de-duplication (sec:comm_allreduce: "our
+ * all-reduce implementation synchronizes instances of each expert class with less inter-node
+ * network traffic").  Bit-identical to the plain path under reading A11:
+ *  - reduce: a GPU holding >= 3 replicas of an expert first sums them locally in fp32, in
+ *    ascending slot order (exactly the per-GPU partial of A11); owners then read that fp32
+ *    partial (4 B/element) instead of the r bf16 slices (2r B/element);
+ *  - place: an owner writes each updated bf16 shard ONCE per destination GPU (its first slot
+ *    of that expert); the destination GPU copies it into its other slots of the expert.
+ * Costs a library-owned fp32 buffer of min(E, S/3) x P per GPU.  Only useful when G > 1.  */
+#define MOE_OPT_DEDUP 1
 
 /* Creates a context (allocates scratch and the sync buffer on desc->device).
  * Virtual mode is ready immediately.  Real mode (G > 1) additionally needs
@@ -151,6 +163,10 @@ int moe_ctx_connect(moe_ctx *ctx, const void *all);
 int moe_ctx_set_timing(moe_ctx *ctx, int32_t enable);
 int moe_ctx_get_timing(moe_ctx *ctx, double *dispatch_ms, int64_t *n_dispatch, double *update_ms,
                        int64_t *n_update);
+/* Finer breakdown (also cleared by either getter): ms[4] / n[4] for the stages
+ * 0 dispatch (3 kernels), 1 update stage (with MOE_OPT_DEDUP: presum + update + replicate;
+ * else the update kernel), 2 k_presum alone, 3 k_replicate alone.                        */
+int moe_ctx_get_timing_ex(moe_ctx *ctx, double *ms, int64_t *n);
 
 /* Synchronises `stream`, then reports and clears device-raised errors
  * (MOE_ERR_DATA, MOE_ERR_TIMEOUT).                                               */

@@ -22,7 +22,7 @@ EXPORTED = [
     "moe_status_str", "moe_last_error", "moe_abi_version", "moe_plan", "moe_plan_ex",
     "moe_ctx_create", "moe_ctx_destroy", "moe_ctx_handle_bytes", "moe_ctx_export",
     "moe_ctx_connect", "moe_ctx_check", "moe_ctx_wait_counts", "moe_dispatch", "moe_update",
-    "moe_place", "moe_step", "moe_ctx_set_timing", "moe_ctx_get_timing",
+    "moe_place", "moe_step", "moe_ctx_set_timing", "moe_ctx_get_timing", "moe_ctx_get_timing_ex",
     "moe_synth_grads", "moe_synth_master",
 ]
 
@@ -42,7 +42,10 @@ class MoeCtxDesc(C.Structure):
                 ("rank", C.c_int32), ("device", C.c_int32),
                 ("slot_w", C.POINTER(C.c_void_p)), ("slot_g", C.POINTER(C.c_void_p)),
                 ("master", C.POINTER(C.c_void_p)), ("adam_m", C.POINTER(C.c_void_p)),
-                ("adam_v", C.POINTER(C.c_void_p))]
+                ("adam_v", C.POINTER(C.c_void_p)), ("options", C.c_int32)]
+
+
+MOE_OPT_DEDUP = 1
 
 
 class MoeDispatchOut(C.Structure):
@@ -105,6 +108,8 @@ def lib() -> C.CDLL:
         L.moe_ctx_get_timing.restype = C.c_int
         L.moe_ctx_get_timing.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64),
                                          C.POINTER(C.c_double), C.POINTER(C.c_int64)]
+        L.moe_ctx_get_timing_ex.restype = C.c_int
+        L.moe_ctx_get_timing_ex.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
         L.moe_update.restype = C.c_int
         L.moe_update.argtypes = [C.c_void_p, C.POINTER(MoePlanT), C.POINTER(MoePlanT),
                                  C.POINTER(MoeAdamT), C.c_void_p]

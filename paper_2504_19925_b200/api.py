@@ -13,7 +13,7 @@ import numpy as np
 import torch
 
 from . import _lib as L
-from ._lib import MOE_PLAN_MINMAX, MOE_PLAN_PAPER_ALG1, MoeError, check  # noqa: F401
+from ._lib import MOE_OPT_DEDUP, MOE_PLAN_MINMAX, MOE_PLAN_PAPER_ALG1, MoeError, check  # noqa: F401
 
 
 def _stream_ptr(stream) -> C.c_void_p:
@@ -84,7 +84,8 @@ class MoeContext:
     """
 
     def __init__(self, E: int, G: int, S: int, k: int, P: int, max_tokens: int, rank: int,
-                 slot_w, slot_g, master, adam_m, adam_v, device: int | None = None):
+                 slot_w, slot_g, master, adam_m, adam_v, device: int | None = None,
+                 options: int = 0):
         n_local = G if rank < 0 else 1
         for name, lst in (("slot_w", slot_w), ("slot_g", slot_g), ("master", master),
                           ("adam_m", adam_m), ("adam_v", adam_v)):
@@ -109,7 +110,8 @@ class MoeContext:
             return a
         self._arrs = [arr(slot_w), arr(slot_g), arr(master), arr(adam_m), arr(adam_v)]
         desc = L.MoeCtxDesc(E, G, S, k, P, max_tokens, rank, self.device,
-                            *[C.cast(a, C.POINTER(C.c_void_p)) for a in self._arrs])
+                            *[C.cast(a, C.POINTER(C.c_void_p)) for a in self._arrs], options)
+        self.options = options
         h = C.c_void_p()
         check(L.lib().moe_ctx_create(C.byref(desc), C.byref(h)), "moe_ctx_create")
         self._h = h
@@ -141,13 +143,13 @@ class MoeContext:
         check(L.lib().moe_ctx_set_timing(self.handle, int(enable)), "moe_ctx_set_timing")
 
     def get_timing(self) -> dict:
-        """Summed CUDA-event ms and launch counts of dispatches / update kernels since last call."""
-        dm, um = C.c_double(), C.c_double()
-        dn, un = C.c_int64(), C.c_int64()
-        check(L.lib().moe_ctx_get_timing(self.handle, C.byref(dm), C.byref(dn), C.byref(um),
-                                         C.byref(un)), "moe_ctx_get_timing")
-        return {"dispatch_ms": dm.value, "n_dispatch": dn.value, "update_ms": um.value,
-                "n_update": un.value}
+        """Summed CUDA-event ms and launch counts per stage since the last call: dispatch,
+        update (stage), presum, replicate."""
+        ms = (C.c_double * 4)()
+        n = (C.c_int64 * 4)()
+        check(L.lib().moe_ctx_get_timing_ex(self.handle, ms, n), "moe_ctx_get_timing_ex")
+        return {"dispatch_ms": ms[0], "n_dispatch": n[0], "update_ms": ms[1], "n_update": n[1],
+                "presum_ms": ms[2], "n_presum": n[2], "replicate_ms": ms[3], "n_replicate": n[3]}
 
     def wait_counts(self) -> None:
         """Host waits for the C_e copy of the last moe_dispatch (not for its scatter)."""

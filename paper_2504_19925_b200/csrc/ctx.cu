@@ -76,8 +76,9 @@ void free_ctx(moe_ctx *c) {
   cudaFree(c->err);
   cudaFree(c->item_ctr);
   cudaFree(c->scan_done);
+  for (float *p : c->presum) cudaFree(p);
   if (c->host_flag) cudaFreeHost((void *)c->host_flag);
-  for (auto *v : {&c->ev_pool, &c->ev_disp, &c->ev_upd})
+  for (auto *v : {&c->ev_pool, &c->ev_disp, &c->ev_upd, &c->ev_presum, &c->ev_repl})
     for (auto &p : *v) {
       cudaEventDestroy(p.first);
       cudaEventDestroy(p.second);
@@ -196,21 +197,39 @@ extern "C" int moe_ctx_create(const moe_ctx_desc *d, moe_ctx **out) {
     const char *k = getenv("MOE_UPDATE_KERNEL");
     c->update_kernel = (k && std::string(k) == "ldg") ? 0 : 1;
   }
+  // locality de-duplication: one fp32 partial-sum buffer per local GPU
+  c->dedup = (d->options & MOE_OPT_DEDUP) && c->G > 1;
+  c->nq_max = std::min(c->E, c->S / 3);
+  if (c->dedup && c->nq_max < 1) c->dedup = false;  // S < 3: no GPU can hold 3 replicas
+  if (c->dedup) {
+    for (int v = 0; v < n_local; ++v) {
+      float *p = nullptr;
+      if (cudaMalloc(&p, sizeof(float) * (size_t)c->nq_max * (size_t)c->P) != cudaSuccess) {
+        cudaGetLastError();
+        free_ctx(c);
+        return fail(MOE_ERR_CUDA, "moe_ctx_create: cannot allocate the de-duplication buffer");
+      }
+      c->presum.push_back(p);
+    }
+  }
   for (int h = 0; h < MOE_MAX_G; ++h) {
     c->peer_slot_g[h] = c->peer_slot_w[h] = nullptr;
     c->peer_sync[h] = nullptr;
+    c->peer_presum[h] = nullptr;
   }
   if (c->rank < 0) {  // virtual: every "peer" is local
     for (int h = 0; h < c->G; ++h) {
       c->peer_slot_g[h] = c->slot_g[h];
       c->peer_slot_w[h] = c->slot_w[h];
       c->peer_sync[h] = c->sync;
+      if (c->dedup) c->peer_presum[h] = c->presum[h];
     }
     c->connected = true;
   } else {
     c->peer_slot_g[c->rank] = c->slot_g[0];
     c->peer_slot_w[c->rank] = c->slot_w[0];
     c->peer_sync[c->rank] = c->sync;
+    if (c->dedup) c->peer_presum[c->rank] = c->presum[0];
     c->connected = (c->G == 1);
   }
   *out = c;
@@ -230,8 +249,11 @@ extern "C" int moe_ctx_export(moe_ctx *ctx, void *out) {
   MOE_CUDA_TRY(cudaSetDevice(ctx->device));
   IpcRecord rec;
   memset(&rec, 0, sizeof(rec));
-  const void *bufs[3] = {ctx->slot_g[0], ctx->slot_w[0], ctx->sync};
-  for (int i = 0; i < 3; ++i) {
+  const void *bufs[4] = {ctx->slot_g[0], ctx->slot_w[0], ctx->sync,
+                         ctx->dedup ? ctx->presum[0] : nullptr};
+  rec.has_presum = ctx->dedup ? 1 : 0;
+  for (int i = 0; i < 4; ++i) {
+    if (!bufs[i]) continue;
     void *base = nullptr;
     int st = alloc_base(bufs[i], &base);
     if (st) return st;
@@ -249,8 +271,10 @@ extern "C" int moe_ctx_connect(moe_ctx *ctx, const void *all) {
   const IpcRecord *recs = (const IpcRecord *)all;
   for (int h = 0; h < ctx->G; ++h) {
     if (h == ctx->rank) continue;
-    void *ptrs[3];
-    for (int i = 0; i < 3; ++i) {
+    if ((recs[h].has_presum != 0) != ctx->dedup)
+      return fail(MOE_ERR_INVALID, "moe_ctx_connect: ranks disagree on MOE_OPT_DEDUP");
+    void *ptrs[4] = {nullptr, nullptr, nullptr, nullptr};
+    for (int i = 0; i < (ctx->dedup ? 4 : 3); ++i) {
       std::string key((const char *)&recs[h].h[i], sizeof(cudaIpcMemHandle_t));
       auto it = ctx->opened.find(key);
       void *base = nullptr;
@@ -268,6 +292,7 @@ extern "C" int moe_ctx_connect(moe_ctx *ctx, const void *all) {
     ctx->peer_slot_g[h] = ptrs[0];
     ctx->peer_slot_w[h] = ptrs[1];
     ctx->peer_sync[h] = (SyncBuf *)ptrs[2];
+    ctx->peer_presum[h] = (float *)ptrs[3];
   }
   ctx->connected = true;
   return MOE_OK;
@@ -298,14 +323,14 @@ extern "C" int moe_ctx_set_timing(moe_ctx *ctx, int32_t enable) {
   return MOE_OK;
 }
 
-extern "C" int moe_ctx_get_timing(moe_ctx *ctx, double *dispatch_ms, int64_t *n_dispatch,
-                                  double *update_ms, int64_t *n_update) {
-  if (!ctx) return fail(MOE_ERR_INVALID, "moe_ctx_get_timing: NULL ctx");
+extern "C" int moe_ctx_get_timing_ex(moe_ctx *ctx, double *ms_out, int64_t *n_out) {
+  if (!ctx || !ms_out || !n_out) return fail(MOE_ERR_INVALID, "moe_ctx_get_timing_ex: NULL argument");
   MOE_CUDA_TRY(cudaSetDevice(ctx->device));
-  double sums[2] = {0.0, 0.0};
-  int64_t counts[2] = {0, 0};
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> *lists[2] = {&ctx->ev_disp, &ctx->ev_upd};
-  for (int k = 0; k < 2; ++k) {
+  double sums[4] = {0.0, 0.0, 0.0, 0.0};
+  int64_t counts[4] = {0, 0, 0, 0};
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> *lists[4] = {&ctx->ev_disp, &ctx->ev_upd,
+                                                                 &ctx->ev_presum, &ctx->ev_repl};
+  for (int k = 0; k < 4; ++k) {
     for (auto &p : *lists[k]) {
       float ms = 0.f;
       MOE_CUDA_TRY(cudaEventSynchronize(p.second));
@@ -316,6 +341,20 @@ extern "C" int moe_ctx_get_timing(moe_ctx *ctx, double *dispatch_ms, int64_t *n_
     }
     lists[k]->clear();
   }
+  for (int k = 0; k < 4; ++k) {
+    ms_out[k] = sums[k];
+    n_out[k] = counts[k];
+  }
+  return MOE_OK;
+}
+
+extern "C" int moe_ctx_get_timing(moe_ctx *ctx, double *dispatch_ms, int64_t *n_dispatch,
+                                  double *update_ms, int64_t *n_update) {
+  if (!ctx) return fail(MOE_ERR_INVALID, "moe_ctx_get_timing: NULL ctx");
+  double sums[4];
+  int64_t counts[4];
+  const int st = moe_ctx_get_timing_ex(ctx, sums, counts);
+  if (st) return st;
   if (dispatch_ms) *dispatch_ms = sums[0];
   if (n_dispatch) *n_dispatch = counts[0];
   if (update_ms) *update_ms = sums[1];

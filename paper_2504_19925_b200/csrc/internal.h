@@ -41,8 +41,10 @@ struct ExpertInfo {
 };
 
 struct IpcRecord {
-  cudaIpcMemHandle_t h[3];  // slot_g, slot_w, sync
-  uint64_t off[3];          // byte offset of the buffer inside its allocation
+  cudaIpcMemHandle_t h[4];  // slot_g, slot_w, sync, presum (zeroed when absent)
+  uint64_t off[4];          // byte offset of the buffer inside its allocation
+  int32_t has_presum;
+  int32_t pad;
 };
 
 }  // namespace moe
@@ -67,6 +69,12 @@ struct moe_ctx {
   void *peer_slot_g[MOE_MAX_G];
   void *peer_slot_w[MOE_MAX_G];
   moe::SyncBuf *peer_sync[MOE_MAX_G];
+  float *peer_presum[MOE_MAX_G];  // fp32 [nq_max][P] local-replica partial sums (dedup)
+
+  // locality de-duplication (MOE_OPT_DEDUP)
+  bool dedup;
+  int nq_max;                  // min(E, S / 3): partial-sum rows per GPU
+  std::vector<float *> presum; // [n_local] library-owned
 
   // library-owned device scratch
   moe::SyncBuf *sync;       // this GPU's sync buffer (virtual mode: the single shared one)
@@ -87,7 +95,7 @@ struct moe_ctx {
 
   // measurement hooks (moe_ctx_set_timing): event pairs per stage, recycled
   bool timing;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool, ev_disp, ev_upd;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool, ev_disp, ev_upd, ev_presum, ev_repl;
 };
 
 namespace moe {

@@ -52,6 +52,10 @@ struct UpdArgs {
   int32_t *err;
   SyncBuf *sync_local;
   SyncBuf *sync_peer[MOE_MAX_G];
+  // locality de-duplication (MOE_OPT_DEDUP)
+  int32_t dedup;
+  int8_t pq[MOE_MAX_E][MOE_MAX_G];  // row of expert e's fp32 partial on GPU h under plan_cur, or -1
+  const float *presum[MOE_MAX_G];   // per GPU h: fp32 [nq_max][P]
 };
 
 __device__ __forceinline__ uint4 ld_stream(const uint16_t *p) {
@@ -91,11 +95,14 @@ constexpr int kBatch = 8;  // replica grad slices loaded per round (16 B each, i
 // at ~46 % of a link at G = 4 even though the total per-GPU volume is balanced (App. E).
 
 // a5: the 16-byte bf16 vector -> every slot j of plan_next hosting e; slot j is on GPU j / S.
-__device__ __forceinline__ void place_to(const UpdArgs &a, int e, int64_t gi, const uint4 &wb) {
+// With de-duplication, a remote GPU only receives it in its first slot of e (j == n0 or
+// l == 0); k_replicate copies it into that GPU's other slots of e afterwards.
+__device__ __forceinline__ void place_to(const UpdArgs &a, int e, int owner, int64_t gi,
+                                         const uint4 &wb) {
   const int n0 = a.fs_next[e], n1 = a.fs_next[e + 1];
   int h = a.h_first_next[e], l = n0 - h * a.S;
   for (int j = n0; j < n1; ++j) {
-    st_stream(a.wbase[h] + (int64_t)l * a.P + gi, wb);
+    if (!a.dedup || h == owner || j == n0 || l == 0) st_stream(a.wbase[h] + (int64_t)l * a.P + gi, wb);
     if (++l == a.S) {
       l = 0;
       ++h;
@@ -140,7 +147,7 @@ __global__ void __launch_bounds__(kThreads) k_update(const __grid_constant__ Upd
                                   bf16_rne_bits(x0.z) | (bf16_rne_bits(x0.w) << 16),
                                   bf16_rne_bits(x1.x) | (bf16_rne_bits(x1.y) << 16),
                                   bf16_rne_bits(x1.z) | (bf16_rne_bits(x1.w) << 16));
-      place_to(a, e, gi, wb);
+      place_to(a, e, o, gi, wb);
       continue;
     }
 
@@ -224,7 +231,7 @@ __global__ void __launch_bounds__(kThreads) k_update(const __grid_constant__ Upd
     pv[1] = make_float4(v[4], v[5], v[6], v[7]);
 
     // a5: push the bf16 vector to every slot of plan_{t+1} hosting e (local or peer HBM)
-    place_to(a, e, gi, wb);
+    place_to(a, e, o, gi, wb);
   }
 }
 
@@ -367,17 +374,31 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_update_tma(const __grid_cons
       }
       const int64_t g0 = (int64_t)o * a.Pg + loc0;
       const int j0 = a.fs_cur[e], j1 = a.fs_cur[e + 1];
-      int h = a.h_first_cur[e], l = j0 - h * a.S;
-      for (int j = j0; j < j1; ++j) {
-        const int g = gi_ % kGradSlots;
-        mbar_wait(gr_empty + g, ((gi_ / kGradSlots) & 1) ^ 1);
-        mbar_expect_tx(gr_full + g, nval * 2);
-        bulk_g2s(grad + (size_t)g * kChunk, a.gbase[h] + (int64_t)l * P + g0, nval * 2, gr_full + g);
-        ++gi_;
-        if (++l == a.S) {
-          l = 0;
-          ++h;
+      for (int h = a.h_first_cur[e], ja = j0; ja < j1; ++h) {  // GPU h's run [ja, jb) of e's slots
+        const int jb = min(j1, (h + 1) * a.S);
+        const int q = a.dedup ? a.pq[e][h] : -1;
+        if (q >= 0) {  // de-dup: GPU h's fp32 partial of this run, as two 4 KB ring slots
+          const float *src = a.presum[h] + (int64_t)q * P + g0;
+          const uint32_t nA = nval < kChunk / 2 ? nval : kChunk / 2, nB = nval - nA;
+          for (int half = 0; half < 2; ++half) {
+            const int g = gi_ % kGradSlots;
+            mbar_wait(gr_empty + g, ((gi_ / kGradSlots) & 1) ^ 1);
+            const uint32_t n = half ? nB : nA;
+            mbar_expect_tx(gr_full + g, n * 4);
+            if (n) bulk_g2s(grad + (size_t)g * kChunk, src + half * (kChunk / 2), n * 4, gr_full + g);
+            ++gi_;
+          }
+        } else {  // one bf16 slice per replica slot
+          for (int j = ja; j < jb; ++j) {
+            const int g = gi_ % kGradSlots;
+            mbar_wait(gr_empty + g, ((gi_ / kGradSlots) & 1) ^ 1);
+            mbar_expect_tx(gr_full + g, nval * 2);
+            bulk_g2s(grad + (size_t)g * kChunk, a.gbase[h] + (int64_t)(j - h * a.S) * P + g0, nval * 2,
+                     gr_full + g);
+            ++gi_;
+          }
         }
+        ja = jb;
       }
     }
     return;
@@ -415,52 +436,64 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_update_tma(const __grid_cons
       ++si;
     }
     // a3: two-level fp32 sum, replica slices in ascending slot order (reading A11)
+    // For each GPU h hosting e (ascending): part = fp32 sum of its replica slices in ascending
+    // slot order (or, de-duplicated, GPU h's precomputed fp32 partial -- the same value);
+    // tot = part_{h0} + part_{h1} + ... in ascending h.
     const int j0 = a.fs_cur[e], j1 = a.fs_cur[e + 1];
     float part[8], tot[8];
     bool have_tot = false;
-    int h = a.h_first_cur[e], l = j0 - h * a.S, cur_h = h;
-    for (int j = j0; j < j1; ++j) {
-      const int g = gi_ % kGradSlots;
-      mbar_wait(gr_full + g, (gi_ / kGradSlots) & 1);
-      if (act) {
-        const uint4 x = *reinterpret_cast<const uint4 *>(grad + (size_t)g * kChunk + tid * kVec);
-        float g8[8];
-        unpack_bf16x8(x, g8);
-        if (j == j0) {
+    for (int h = a.h_first_cur[e], ja = j0; ja < j1; ++h) {
+      const int jb = min(j1, (h + 1) * a.S);
+      const int q = a.dedup ? a.pq[e][h] : -1;
+      if (q >= 0) {
+        const int gA = gi_ % kGradSlots, gB = (gi_ + 1) % kGradSlots;
+        mbar_wait(gr_full + gA, (gi_ / kGradSlots) & 1);
+        mbar_wait(gr_full + gB, ((gi_ + 1) / kGradSlots) & 1);
+        if (act) {
+          const int half = tid >= kThreads / 2;
+          const float *src = reinterpret_cast<const float *>(grad + (size_t)(half ? gB : gA) * kChunk) +
+                             (tid - half * (kThreads / 2)) * kVec;
+          const float4 x0 = *reinterpret_cast<const float4 *>(src);
+          const float4 x1 = *reinterpret_cast<const float4 *>(src + 4);
+          part[0] = x0.x; part[1] = x0.y; part[2] = x0.z; part[3] = x0.w;
+          part[4] = x1.x; part[5] = x1.y; part[6] = x1.z; part[7] = x1.w;
+        }
+        release_slot(gr_empty + gA, lane);
+        release_slot(gr_empty + gB, lane);
+        gi_ += 2;
+      } else {
+        for (int j = ja; j < jb; ++j) {
+          const int g = gi_ % kGradSlots;
+          mbar_wait(gr_full + g, (gi_ / kGradSlots) & 1);
+          if (act) {
+            const uint4 x = *reinterpret_cast<const uint4 *>(grad + (size_t)g * kChunk + tid * kVec);
+            float g8[8];
+            unpack_bf16x8(x, g8);
+            if (j == ja) {
 #pragma unroll
-          for (int i = 0; i < 8; ++i) part[i] = g8[i];
-        } else if (h != cur_h) {  // next GPU: fold the finished per-GPU partial into tot
-          if (have_tot) {
+              for (int i = 0; i < 8; ++i) part[i] = g8[i];
+            } else {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) tot[i] = __fadd_rn(tot[i], part[i]);
-          } else {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) tot[i] = part[i];
+              for (int i = 0; i < 8; ++i) part[i] = __fadd_rn(part[i], g8[i]);
+            }
           }
-          have_tot = true;
-#pragma unroll
-          for (int i = 0; i < 8; ++i) part[i] = g8[i];
-          cur_h = h;
-        } else {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) part[i] = __fadd_rn(part[i], g8[i]);
+          release_slot(gr_empty + g, lane);
+          ++gi_;
         }
       }
-      release_slot(gr_empty + g, lane);
-      ++gi_;
-      if (++l == a.S) {
-        l = 0;
-        ++h;
+      if (act) {  // fold GPU h's partial into the total
+        if (have_tot) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) tot[i] = __fadd_rn(tot[i], part[i]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) tot[i] = part[i];
+        }
       }
+      have_tot = true;
+      ja = jb;
     }
     if (!act) continue;
-    if (have_tot) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) tot[i] = __fadd_rn(tot[i], part[i]);
-    } else {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) tot[i] = part[i];
-    }
     uint4 wb;
     adam8(a, tot, a.scale[e], w, m, v, wb);                              // a4
     const int64_t so = (int64_t)e * a.Pg + loc;
@@ -473,7 +506,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_update_tma(const __grid_cons
     pm[1] = make_float4(m[4], m[5], m[6], m[7]);
     pv[0] = make_float4(v[0], v[1], v[2], v[3]);
     pv[1] = make_float4(v[4], v[5], v[6], v[7]);
-    place_to(a, e, (int64_t)o * a.Pg + loc, wb);                          // a5
+    place_to(a, e, o, (int64_t)o * a.Pg + loc, wb);                       // a5
   }
 
   // Barrier-out (real mode): "every push into every GPU's slots has landed".  Each consumer
@@ -489,6 +522,96 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_update_tma(const __grid_cons
       for (int h = 0; h < a.G; ++h) st_release_sys(&a.sync_peer[h]->upd_out[a.rank], a.epoch);
       for (int h = 0; h < a.G; ++h) wait_flag(&a.sync_local->upd_out[h], a.epoch, a.err);
     }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Locality de-duplication (MOE_OPT_DEDUP).
+// k_presum: on each GPU h, for every expert e with >= 3 replicas on h under plan_cur, the
+//   fp32 sum of those replicas' bf16 grads in ascending slot order over all P elements --
+//   exactly GPU h's partial of reading A11, so owners reading it instead of the slices get
+//   identical bits.  Runs before k_update_tma (whose barrier-in then also covers it).
+// k_replicate: on each GPU h, after k_update_tma (whose barrier-out guarantees every push has
+//   landed), copies the remote owners' element ranges from h's first slot of an expert into
+//   h's other slots of that expert under plan_next (the owners pushed only to the first one).
+// ------------------------------------------------------------------------------------------
+struct PresumArgs {
+  int32_t S, o_begin, nq_total;
+  int64_t P, nchunks;                 // kChunk-element chunks over the full [0, P)
+  int32_t qoff[MOE_MAX_G + 1];        // prefix of partial rows over local ranks
+  int16_t q_e[MOE_MAX_G][MOE_MAX_E];  // expert of partial row q of local rank v
+  int32_t fs[MOE_MAX_E + 1];          // plan_cur
+  const uint16_t *grads[MOE_MAX_G];   // local rank v: bf16 [S][P]
+  float *presum[MOE_MAX_G];           // local rank v: fp32 [nq_max][P]
+};
+
+__global__ void __launch_bounds__(kThreads) k_presum(const __grid_constant__ PresumArgs a) {
+  const int64_t total = (int64_t)a.nq_total * a.nchunks;
+  for (int64_t it = blockIdx.x; it < total; it += gridDim.x) {
+    const int row = (int)(it / a.nchunks);
+    const int64_t c = it - (int64_t)row * a.nchunks;
+    int v = 0;
+    while (row >= a.qoff[v + 1]) ++v;
+    const int q = row - a.qoff[v];
+    const int e = a.q_e[v][q];
+    const int h = a.o_begin + v;
+    const int ja = max(a.fs[e], h * a.S), jb = min(a.fs[e + 1], (h + 1) * a.S);
+    const int64_t i = c * kChunk + (int64_t)threadIdx.x * kVec;
+    if (i >= a.P) continue;
+    const uint16_t *base = a.grads[v] + i;
+    float part[8];
+    for (int j = ja; j < jb; j += kBatch) {  // ascending slot order, loads batched
+      const int n = min(kBatch, jb - j);
+      uint4 buf[kBatch];
+#pragma unroll
+      for (int b = 0; b < kBatch; ++b)
+        if (b < n) buf[b] = ld_stream(base + (int64_t)(j + b - h * a.S) * a.P);
+#pragma unroll
+      for (int b = 0; b < kBatch; ++b)
+        if (b < n) {
+          float g8[8];
+          unpack_bf16x8(buf[b], g8);
+          if (j + b == ja) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) part[k] = g8[k];
+          } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) part[k] = __fadd_rn(part[k], g8[k]);
+          }
+        }
+    }
+    float4 *dst = reinterpret_cast<float4 *>(a.presum[v] + (int64_t)q * a.P + i);
+    dst[0] = make_float4(part[0], part[1], part[2], part[3]);
+    dst[1] = make_float4(part[4], part[5], part[6], part[7]);
+  }
+}
+
+struct ReplArgs {
+  int32_t E, S, o_begin;
+  int64_t P, Pg;
+  int32_t fs[MOE_MAX_E + 1];  // plan_next
+  uint16_t *w[MOE_MAX_G];     // local rank v: bf16 slot weights [S][P]
+};
+
+__global__ void __launch_bounds__(kThreads) k_replicate(const __grid_constant__ ReplArgs a) {
+  const int v = blockIdx.y / a.S, l = blockIdx.y % a.S;
+  const int h = a.o_begin + v;
+  const int j = h * a.S + l;
+  int lo = 0, hi = a.E - 1;  // expert of global slot j: largest e with fs[e] <= j
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (a.fs[mid] <= j) lo = mid;
+    else hi = mid - 1;
+  }
+  const int j0 = max(a.fs[lo], h * a.S);  // GPU h's first slot of that expert
+  if (j == j0) return;
+  const uint16_t *src = a.w[v] + (int64_t)(j0 - h * a.S) * a.P;
+  uint16_t *dst = a.w[v] + (int64_t)l * a.P;
+  const int64_t nrem = a.P - a.Pg, own = (int64_t)h * a.Pg;  // remote owners' elements
+  for (int64_t r = ((int64_t)blockIdx.x * kThreads + threadIdx.x) * kVec; r < nrem;
+       r += (int64_t)gridDim.x * kThreads * kVec) {
+    const int64_t i = r < own ? r : r + a.Pg;
+    st_stream(dst + i, ld_stream(src + i));
   }
 }
 
@@ -601,7 +724,48 @@ int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *pl
   a.item_ctr = ctx->item_ctr;
   const bool multi = ctx->rank >= 0 && ctx->G > 1;
   const uint32_t epoch = ++ctx->upd_epoch;
-  const bool tma = !place_only && ctx->update_kernel != 0;
+  const bool dedup = ctx->dedup && !place_only;
+  const bool tma = !place_only && (ctx->update_kernel != 0 || dedup);  // de-dup needs the TMA kernel
+  a.dedup = dedup ? 1 : 0;
+  std::pair<cudaEvent_t, cudaEvent_t> stage_ev{nullptr, nullptr};
+  memset(a.pq, -1, sizeof(a.pq));
+  PresumArgs pa{};
+  if (dedup) {  // partial rows: for each GPU h, experts with >= 3 replicas on h, ascending
+    pa.S = ctx->S;
+    pa.o_begin = a.o_begin;
+    pa.P = ctx->P;
+    pa.nchunks = (ctx->P + kChunk - 1) / kChunk;
+    for (int e = 0; e <= ctx->E; ++e) pa.fs[e] = plan_cur->first_slot[e];
+    for (int h = 0; h < ctx->G; ++h) {
+      int nq = 0;
+      for (int e = 0; e < ctx->E; ++e) {
+        const int ja = std::max(pa.fs[e], h * ctx->S), jb = std::min(pa.fs[e + 1], (h + 1) * ctx->S);
+        if (jb - ja >= 3) {
+          a.pq[e][h] = (int8_t)nq;
+          const int v = h - a.o_begin;
+          if (v >= 0 && v < ctx->n_local) pa.q_e[v][nq] = (int16_t)e;
+          ++nq;
+        }
+      }
+      if (nq > ctx->nq_max) return fail(MOE_ERR_INTERNAL, "de-dup: %d partial rows > %d", nq, ctx->nq_max);
+      const int v = h - a.o_begin;
+      if (v >= 0 && v < ctx->n_local) pa.qoff[v + 1] = pa.qoff[v] + nq;
+    }
+    pa.nq_total = pa.qoff[ctx->n_local];
+    for (int v = 0; v < ctx->n_local; ++v) {
+      pa.grads[v] = (const uint16_t *)ctx->slot_g[v];
+      pa.presum[v] = ctx->presum[v];
+    }
+    for (int h = 0; h < ctx->G; ++h) a.presum[h] = ctx->peer_presum[h];
+    stage_ev = timing_begin(ctx, s);  // with de-dup the timed "update" is the whole stage
+    if (pa.nq_total > 0) {
+      const int64_t grid = std::min<int64_t>((int64_t)pa.nq_total * pa.nchunks, (int64_t)ctx->num_sms * 8);
+      const auto pev = timing_begin(ctx, s);
+      k_presum<<<(unsigned)grid, kThreads, 0, s>>>(pa);
+      MOE_CUDA_TRY(cudaGetLastError());
+      timing_end(ctx->ev_presum, pev, s);
+    }
+  }
   a.fused_barrier = (multi && tma) ? 1 : 0;  // k_update_tma carries both barriers itself
   a.rank = ctx->rank;
   a.epoch = epoch;
@@ -621,7 +785,7 @@ int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *pl
     MOE_CUDA_TRY(cudaGetLastError());
   }
   const int64_t items = (int64_t)ctx->E * a.nchunks * a.o_count;
-  if (place_only || ctx->update_kernel == 0) {
+  if (!tma) {
     const int64_t grid = std::min<int64_t>(items, (int64_t)ctx->num_sms * ctx->upd_blocks_per_sm);
     if (grid > 0) {
       const auto tev = place_only ? std::pair<cudaEvent_t, cudaEvent_t>{nullptr, nullptr}
@@ -633,7 +797,7 @@ int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *pl
   } else {
     const int64_t grid = std::min<int64_t>(items, (int64_t)ctx->num_sms * 2);
     if (grid > 0) {
-      const auto tev = timing_begin(ctx, s);
+      const auto tev = dedup ? std::pair<cudaEvent_t, cudaEvent_t>{nullptr, nullptr} : timing_begin(ctx, s);
       k_update_tma<<<(unsigned)grid, kTmaThreads, kTmaSmem, s>>>(a);
       MOE_CUDA_TRY(cudaGetLastError());
       timing_end(ctx->ev_upd, tev, s);
@@ -643,6 +807,33 @@ int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *pl
     ba.which = 1;
     k_barrier<<<1, 32, 0, s>>>(ba);
     MOE_CUDA_TRY(cudaGetLastError());
+  }
+  if (dedup) {  // fill this GPU's duplicate slots of plan_next from its first slot of each expert
+    ReplArgs ra{};
+    ra.E = ctx->E;
+    ra.S = ctx->S;
+    ra.o_begin = a.o_begin;
+    ra.P = ctx->P;
+    ra.Pg = ctx->Pg;
+    for (int e = 0; e <= ctx->E; ++e) ra.fs[e] = plan_next->first_slot[e];
+    int ndup = 0;
+    for (int v = 0; v < ctx->n_local; ++v) {
+      ra.w[v] = (uint16_t *)ctx->slot_w[v];
+      const int h = a.o_begin + v;
+      for (int e = 0; e < ctx->E; ++e) {
+        const int ja = std::max(ra.fs[e], h * ctx->S), jb = std::min(ra.fs[e + 1], (h + 1) * ctx->S);
+        if (jb - ja > 1) ndup += jb - ja - 1;
+      }
+    }
+    if (ndup > 0) {
+      const int gx = std::max(1, std::min<int>((int)((ctx->P - ctx->Pg) / (kThreads * kVec)) + 1,
+                                               4 * ctx->num_sms / ndup + 1));
+      const auto rev = timing_begin(ctx, s);
+      k_replicate<<<dim3(gx, ctx->n_local * ctx->S), kThreads, 0, s>>>(ra);
+      MOE_CUDA_TRY(cudaGetLastError());
+      timing_end(ctx->ev_repl, rev, s);
+    }
+    timing_end(ctx->ev_upd, stage_ev, s);
   }
   return MOE_OK;
 }

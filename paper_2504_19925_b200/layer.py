@@ -23,7 +23,7 @@ class DecoupledExpertLayer:
     def __init__(self, E: int, G: int, S: int, k: int, P: int, max_tokens: int, rank: int = -1,
                  device: int | None = None, seed: int = 0, adam: api.AdamConfig | None = None,
                  policy: int = api.MOE_PLAN_PAPER_ALG1, scale_mode: int = 0, scale=None,
-                 init_master: bool = True):
+                 init_master: bool = True, dedup: bool = False):
         if device is None:
             device = torch.cuda.current_device()
         self.E, self.G, self.S, self.k, self.P = E, G, S, k, P
@@ -42,7 +42,9 @@ class DecoupledExpertLayer:
         self.adam_m = [torch.zeros(E * self.Pg, dtype=torch.float32, device=dev) for _ in range(n)]
         self.adam_v = [torch.zeros(E * self.Pg, dtype=torch.float32, device=dev) for _ in range(n)]
         self.ctx = api.MoeContext(E, G, S, k, P, max_tokens, rank, self.slot_w, self.slot_g,
-                                  self.master, self.adam_m, self.adam_v, device=device)
+                                  self.master, self.adam_m, self.adam_v, device=device,
+                                  options=api.MOE_OPT_DEDUP if dedup else 0)
+        self.dedup = dedup
         self.out = api.DispatchBuffers(self.ctx, max_tokens)
         self.seed = seed
         if init_master:

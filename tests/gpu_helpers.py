@@ -15,7 +15,8 @@ def _u32(x: np.ndarray) -> np.ndarray:
 
 def run_parity(name: str, G: int, iters: int, *, rank_mode: str = "virtual", idx=None,
                T: int | None = None, policy: int = 0, scale_mode: int = 0, scale=None,
-               weight_decay: float = 0.0, trace=None, check_dispatch: bool = True):
+               weight_decay: float = 0.0, trace=None, check_dispatch: bool = True,
+               dedup: bool = False):
     """Returns the number of iterations compared.  rank_mode: "virtual" (rank=-1, G ranks on
     cuda:0) or "single" (real mode with G == 1)."""
     from paper_2504_19925_b200 import AdamConfig, DecoupledExpertLayer
@@ -35,7 +36,7 @@ def run_parity(name: str, G: int, iters: int, *, rank_mode: str = "virtual", idx
     adam = AdamConfig(lr=hyper.lr, beta1=hyper.beta1, beta2=hyper.beta2, eps=hyper.eps,
                       weight_decay=weight_decay)
     layer = DecoupledExpertLayer(E, G, S, k, P, Tg, rank=rank, device=0, seed=seed, adam=adam,
-                                 policy=policy, scale_mode=scale_mode, scale=scale)
+                                 policy=policy, scale_mode=scale_mode, scale=scale, dedup=dedup)
     pol = "alg1" if policy == 0 else "minmax"
     idx_arr = np.arange(P, dtype=np.int64) if idx is None else np.asarray(idx, dtype=np.int64)
     sim = ostep.OracleSim(E, G, S, P, seed, hyper=hyper, policy=pol, scale_mode=scale_mode,

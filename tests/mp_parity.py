@@ -27,6 +27,7 @@ def main() -> int:
     ap.add_argument("--iters", type=int, default=6)
     ap.add_argument("--sampled", action="store_true", help="compare a sample of elements only")
     ap.add_argument("--trace", default="config", choices=["config", "rotating-hot"])
+    ap.add_argument("--dedup", action="store_true", help="MOE_OPT_DEDUP (row f1)")
     args = ap.parse_args()
     rank, G, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -45,7 +46,8 @@ def main() -> int:
     Tg = wl.tokens_per_rank(G)
     Pg = P // G
     seed = configs.seed_for(wl.name)
-    layer = DecoupledExpertLayer(E, G, S, k, P, Tg, rank=rank, device=local, seed=seed)
+    layer = DecoupledExpertLayer(E, G, S, k, P, Tg, rank=rank, device=local, seed=seed,
+                                 dedup=args.dedup)
     layer.connect()
     if args.sampled:
         rng = np.random.default_rng(1)

@@ -81,6 +81,16 @@ def test_edge_cases_empty_and_degenerate():
         run_parity("tiny-skew", 4, 1, trace=[(ids, gates)], T=ids.shape[0])
 
 
+@pytest.mark.parametrize("name,G,iters,sampled", [("tiny-skew", 4, 20, False), ("medium", 4, 6, False),
+                                                  ("medium", 2, 4, False), ("gpt-small", 8, 2, True)])
+def test_dedup_is_bit_identical(name, G, iters, sampled):
+    """Locality de-duplication (row f1): local fp32 partials + once-per-GPU pushes +
+    local replication give exactly the oracle's bits (reading A11 makes them identical)."""
+    from gpu_helpers import run_parity
+    wl = configs.CONFIGS[name]
+    run_parity(name, G, iters, dedup=True, idx=_sample_idx(wl.P, G) if sampled else None)
+
+
 def test_split_calls_equal_native_step_and_timing_hooks():
     """moe_step (native a0..a5) == moe_dispatch + moe_ctx_wait_counts + moe_plan + moe_update,
     bitwise; the timing hooks count one dispatch and one update launch per iteration."""

@@ -29,6 +29,9 @@ def _torchrun(n: int, *args, timeout=600):
 @pytest.mark.parametrize("G,config,extra", [
     (2, "tiny-skew", []), (2, "tiny", []), (4, "tiny-skew", []), (4, "tiny", ["--trace", "rotating-hot"]),
     (2, "gpt-small", ["--sampled", "--iters", "3"]), (8, "gpt-small", ["--sampled", "--iters", "3"]),
+    (2, "medium", ["--dedup", "--iters", "4"]), (4, "medium", ["--dedup", "--iters", "4"]),
+    (4, "tiny-skew", ["--dedup", "--trace", "rotating-hot"]),
+    (4, "gpt-small", ["--dedup", "--sampled", "--iters", "3"]),
 ])
 def test_real_multi_gpu_parity(G, config, extra):
     if torch.cuda.device_count() < G:
