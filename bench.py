@@ -92,10 +92,12 @@ class ClockSampler:
                 "reasons": sorted(reasons)}
 
 
-def update_stage_bytes(fs_cur, fs_next, G: int, S: int, P: int, E: int, dedup: bool):
+def update_stage_bytes(fs_cur, fs_next, G: int, S: int, P: int, E: int, dedup: bool,
+                       parts: bool = False):
     """Algorithmic bytes of one update stage, from the two plans.
 
-    Returns (max over GPUs of HBM bytes, max over GPUs and directions of NVLink bytes).
+    Returns (max over GPUs of HBM bytes, max over GPUs and directions of NVLink bytes); with
+    parts=True a dict that also splits the HBM bytes by kernel (update / presum / replicate).
     Plain path: owner g reads its Pg slice of every replica of e from the GPU holding it and
     writes its bf16 slice into every next-plan slot of e; GPU g also reads+writes its
     master/m/v (24 B/element).  At G = 1 this is 2*S*P + 24*E*P + 2*S*P, and the NVLink bytes
@@ -105,7 +107,8 @@ def update_stage_bytes(fs_cur, fs_next, G: int, S: int, P: int, E: int, dedup: b
     and copies it into its other slots of e (read + write of the remote owners' ranges).
     """
     Pg = P // G
-    hbm = [24 * E * Pg] * G
+    upd = [24 * E * Pg] * G
+    pre, rep = [0] * G, [0] * G
     nin, nout = [0] * G, [0] * G
     for e in range(E):
         for h in range(G):
@@ -114,10 +117,10 @@ def update_stage_bytes(fs_cur, fs_next, G: int, S: int, P: int, E: int, dedup: b
                 continue
             partial = dedup and r >= 3
             if partial:
-                hbm[h] += 2 * r * P + 4 * P
+                pre[h] += 2 * r * P + 4 * P
             per_owner = 4 * Pg if partial else 2 * r * Pg
             for g in range(G):
-                hbm[h] += per_owner
+                upd[h] += per_owner
                 if g != h:
                     nout[h] += per_owner
                     nin[g] += per_owner
@@ -127,13 +130,18 @@ def update_stage_bytes(fs_cur, fs_next, G: int, S: int, P: int, E: int, dedup: b
                 continue
             for g in range(G):
                 n = r if (not dedup or g == h) else 1
-                hbm[h] += 2 * Pg * n
+                upd[h] += 2 * Pg * n
                 if g != h:
                     nout[g] += 2 * Pg * n
                     nin[h] += 2 * Pg * n
             if dedup and r > 1:
-                hbm[h] += (r - 1) * 2 * 2 * (P - Pg)
-    return max(hbm), max(max(nin), max(nout))
+                rep[h] += (r - 1) * 2 * 2 * (P - Pg)
+    hbm = max(u + p + q for u, p, q in zip(upd, pre, rep))
+    nvl = max(max(nin), max(nout))
+    if parts:
+        return {"stage_hbm": hbm, "nvl": nvl, "update_hbm": max(upd), "presum_hbm": max(pre),
+                "replicate_hbm": max(rep)}
+    return hbm, nvl
 
 
 # ------------------------------------------------------------------------------------------
@@ -287,11 +295,12 @@ def gpu_arm(args, wl):
     disp_avg_local = tm["dispatch_ms"] / max(1, tm["n_dispatch"])
     pre_avg_local = tm["presum_ms"] / K
     rep_avg_local = tm["replicate_ms"] / K
-    t = torch.tensor([total_ms, upd_avg_local, disp_avg_local, pre_avg_local, rep_avg_local],
-                     device="cuda")
+    updk_avg_local = tm["update_kernel_ms"] / max(1, tm["n_update_kernel"])
+    t = torch.tensor([total_ms, upd_avg_local, disp_avg_local, pre_avg_local, rep_avg_local,
+                      updk_avg_local], device="cuda")
     if G > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms, upd_avg, disp_avg, pre_avg, rep_avg = (float(x) for x in t.tolist())
+    total_ms, upd_avg, disp_avg, pre_avg, rep_avg, updk_avg = (float(x) for x in t.tolist())
     host_ms = 1e3 * (h1 - h0) / K
     ms_iter = total_ms / K
 
@@ -332,35 +341,31 @@ def gpu_arm(args, wl):
             args.traffic = tj.get(f"{wl.name}/G={G}/k_update_tma", {}).get("dram_bytes")
         except Exception:
             args.traffic = None
-    # algorithmic bytes of the update stage, per timed iteration from the actual plans
-    hbm_b, nvl_b = [], []
-    for fc, fn in plans:
-        hb, nb = update_stage_bytes(fc, fn, G, S, wl.P, wl.E, args.dedup)
-        hbm_b.append(hb)
-        nvl_b.append(nb)
-    upd_hbm = statistics.mean(hbm_b)
-    upd_nvl = statistics.mean(nvl_b)
-    t_hbm = upd_hbm / (peak_hbm * 1e9)
-    t_nvl = upd_nvl / (GUIDE_NVLINK_GBS * 1e9) if G > 1 else 0.0
-    kname = ("update stage (k_presum + k_update_tma + k_replicate)" if args.dedup
-             else "k_update_tma (fused reduce+Adam+place)")
-    if t_nvl > t_hbm:
-        achieved = upd_nvl / (upd_avg * 1e-3) / 1e9
+    # algorithmic bytes, per timed iteration from the actual plans
+    acc = [update_stage_bytes(fc, fn, G, S, wl.P, wl.E, args.dedup, parts=True) for fc, fn in plans]
+    mean = {k: statistics.mean(a[k] for a in acc) for k in acc[0]}
+    # roofline of the dominant kernel, k_update_tma alone (its own HBM and NVLink bytes)
+    t_hbm_k = mean["update_hbm"] / (peak_hbm * 1e9)
+    t_nvl = mean["nvl"] / (GUIDE_NVLINK_GBS * 1e9) if G > 1 else 0.0
+    kname = "k_update_tma (fused reduce+Adam+place" + (", de-dup)" if args.dedup else ")")
+    if t_nvl > t_hbm_k:
+        achieved = mean["nvl"] / (updk_avg * 1e-3) / 1e9
         roof = {"kernel": kname + ", NVLink pulls/pushes", "bound": "nvlink",
                 "achieved": round(achieved, 1), "peak": GUIDE_NVLINK_GBS, "unit": "GB/s",
                 "frac": round(achieved / GUIDE_NVLINK_GBS, 4), "traffic": None,
-                "algorithmic_bytes_per_launch": int(upd_nvl),
+                "algorithmic_bytes_per_launch": int(mean["nvl"]),
                 "peak_source": "B200_PROFILING.md measured peer copy per direction (900 nominal)",
-                "avg_launch_ms": round(upd_avg, 4)}
+                "avg_launch_ms": round(updk_avg, 4)}
     else:
-        achieved = upd_hbm / (upd_avg * 1e-3) / 1e9
+        achieved = mean["update_hbm"] / (updk_avg * 1e-3) / 1e9
         roof = {"kernel": kname, "bound": "hbm", "achieved": round(achieved, 1), "peak": peak_hbm,
                 "unit": "GB/s", "frac": round(achieved / peak_hbm, 4),
                 "traffic": args.traffic if (G == 1 and not args.dedup) else None,
-                "algorithmic_bytes_per_launch": int(upd_hbm), "peak_source": peak_src,
-                "avg_launch_ms": round(upd_avg, 4)}
+                "algorithmic_bytes_per_launch": int(mean["update_hbm"]), "peak_source": peak_src,
+                "avg_launch_ms": round(updk_avg, 4)}
     disp_hbm = 28 * (wl.T // G) * wl.k
-    t_roof_step = max((upd_hbm + disp_hbm) / (peak_hbm * 1e9), t_nvl)
+    # whole step: every HBM byte of dispatch + update stage at the HBM peak, or the NVLink bytes
+    t_roof_step = max((mean["stage_hbm"] + disp_hbm) / (peak_hbm * 1e9), t_nvl)
     launches_per_step = 3 + 1 + (2 if args.dedup else 0)
 
     cpu = None
@@ -380,6 +385,7 @@ def gpu_arm(args, wl):
                               "frac": round(t_roof_step * 1e3 / ms_iter, 4),
                               "basis": "max(HBM bytes of dispatch+update / peak HBM, NVLink bytes/dir / 770 GB/s)"},
             "stages_ms": {"dispatch": round(disp_avg, 4), "update_stage": round(upd_avg, 4),
+                          "update_kernel": round(updk_avg, 4),
                           "presum": round(pre_avg, 4), "replicate": round(rep_avg, 4),
                           "host_enqueue_per_step": round(host_ms, 4),
                           "note": "library CUDA events (moe_ctx_set_timing) on the launching stream: "
@@ -405,8 +411,9 @@ def main():
     ap.add_argument("--trace-iters", type=int, default=25)
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--dedup", action="store_true",
-                    help="locality de-duplication (MOE_OPT_DEDUP, SURVEY row f1); G > 1 only")
+    ap.add_argument("--dedup", default="auto", choices=["auto", "on", "off"],
+                    help="locality de-duplication (MOE_OPT_DEDUP, SURVEY row f1): auto = on when "
+                         "G > 1 (it moves fewer NVLink bytes; bit-identical results)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-iters", type=int, default=3)
     ap.add_argument("--cpu-frac", type=int, default=64)
@@ -415,8 +422,8 @@ def main():
                     help="dram bytes per k_update launch from an ncu --set full capture")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
-    if args.gpus == 1:
-        args.dedup = False  # nothing crosses NVLink at G = 1; the library ignores it too
+    # nothing crosses NVLink at G = 1 (the library ignores the option there too)
+    args.dedup = args.gpus > 1 and args.dedup in ("auto", "on")
     from synth import configs
     wl = configs.CONFIGS[args.config]
     if args.impl == "reference":

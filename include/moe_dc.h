@@ -163,9 +163,17 @@ int moe_ctx_connect(moe_ctx *ctx, const void *all);
 int moe_ctx_set_timing(moe_ctx *ctx, int32_t enable);
 int moe_ctx_get_timing(moe_ctx *ctx, double *dispatch_ms, int64_t *n_dispatch, double *update_ms,
                        int64_t *n_update);
-/* Finer breakdown (also cleared by either getter): ms[4] / n[4] for the stages
- * 0 dispatch (3 kernels), 1 update stage (with MOE_OPT_DEDUP: presum + update + replicate;
- * else the update kernel), 2 k_presum alone, 3 k_replicate alone.                        */
+/* Finer breakdown (also cleared by either getter): ms[MOE_TIMING_STAGES] / n[...] for
+ * MOE_T_DISPATCH (3 kernels), MOE_T_UPDATE (the update kernel alone), MOE_T_PRESUM and
+ * MOE_T_REPLICATE (de-dup kernels), MOE_T_STAGE (the whole update stage: presum + update +
+ * replicate; equals MOE_T_UPDATE without de-dup).  moe_ctx_get_timing's update_ms is
+ * MOE_T_STAGE.                                                                             */
+#define MOE_T_DISPATCH 0
+#define MOE_T_UPDATE 1
+#define MOE_T_PRESUM 2
+#define MOE_T_REPLICATE 3
+#define MOE_T_STAGE 4
+#define MOE_TIMING_STAGES 5
 int moe_ctx_get_timing_ex(moe_ctx *ctx, double *ms, int64_t *n);
 
 /* Synchronises `stream`, then reports and clears device-raised errors

@@ -145,11 +145,12 @@ class MoeContext:
     def get_timing(self) -> dict:
         """Summed CUDA-event ms and launch counts per stage since the last call: dispatch,
         update (stage), presum, replicate."""
-        ms = (C.c_double * 4)()
-        n = (C.c_int64 * 4)()
+        ms = (C.c_double * 5)()
+        n = (C.c_int64 * 5)()
         check(L.lib().moe_ctx_get_timing_ex(self.handle, ms, n), "moe_ctx_get_timing_ex")
-        return {"dispatch_ms": ms[0], "n_dispatch": n[0], "update_ms": ms[1], "n_update": n[1],
-                "presum_ms": ms[2], "n_presum": n[2], "replicate_ms": ms[3], "n_replicate": n[3]}
+        return {"dispatch_ms": ms[0], "n_dispatch": n[0], "update_kernel_ms": ms[1],
+                "n_update_kernel": n[1], "presum_ms": ms[2], "n_presum": n[2],
+                "replicate_ms": ms[3], "n_replicate": n[3], "update_ms": ms[4], "n_update": n[4]}
 
     def wait_counts(self) -> None:
         """Host waits for the C_e copy of the last moe_dispatch (not for its scatter)."""

@@ -78,7 +78,7 @@ void free_ctx(moe_ctx *c) {
   cudaFree(c->scan_done);
   for (float *p : c->presum) cudaFree(p);
   if (c->host_flag) cudaFreeHost((void *)c->host_flag);
-  for (auto *v : {&c->ev_pool, &c->ev_disp, &c->ev_upd, &c->ev_presum, &c->ev_repl})
+  for (auto *v : {&c->ev_pool, &c->ev_disp, &c->ev_upd, &c->ev_presum, &c->ev_repl, &c->ev_stage})
     for (auto &p : *v) {
       cudaEventDestroy(p.first);
       cudaEventDestroy(p.second);
@@ -326,11 +326,11 @@ extern "C" int moe_ctx_set_timing(moe_ctx *ctx, int32_t enable) {
 extern "C" int moe_ctx_get_timing_ex(moe_ctx *ctx, double *ms_out, int64_t *n_out) {
   if (!ctx || !ms_out || !n_out) return fail(MOE_ERR_INVALID, "moe_ctx_get_timing_ex: NULL argument");
   MOE_CUDA_TRY(cudaSetDevice(ctx->device));
-  double sums[4] = {0.0, 0.0, 0.0, 0.0};
-  int64_t counts[4] = {0, 0, 0, 0};
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> *lists[4] = {&ctx->ev_disp, &ctx->ev_upd,
-                                                                 &ctx->ev_presum, &ctx->ev_repl};
-  for (int k = 0; k < 4; ++k) {
+  double sums[MOE_TIMING_STAGES] = {0.0};
+  int64_t counts[MOE_TIMING_STAGES] = {0};
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> *lists[MOE_TIMING_STAGES] = {
+      &ctx->ev_disp, &ctx->ev_upd, &ctx->ev_presum, &ctx->ev_repl, &ctx->ev_stage};
+  for (int k = 0; k < MOE_TIMING_STAGES; ++k) {
     for (auto &p : *lists[k]) {
       float ms = 0.f;
       MOE_CUDA_TRY(cudaEventSynchronize(p.second));
@@ -341,7 +341,12 @@ extern "C" int moe_ctx_get_timing_ex(moe_ctx *ctx, double *ms_out, int64_t *n_ou
     }
     lists[k]->clear();
   }
-  for (int k = 0; k < 4; ++k) {
+  // without de-dup the stage is the update kernel itself
+  if (counts[MOE_T_STAGE] == 0) {
+    sums[MOE_T_STAGE] = sums[MOE_T_UPDATE];
+    counts[MOE_T_STAGE] = counts[MOE_T_UPDATE];
+  }
+  for (int k = 0; k < MOE_TIMING_STAGES; ++k) {
     ms_out[k] = sums[k];
     n_out[k] = counts[k];
   }
@@ -351,14 +356,14 @@ extern "C" int moe_ctx_get_timing_ex(moe_ctx *ctx, double *ms_out, int64_t *n_ou
 extern "C" int moe_ctx_get_timing(moe_ctx *ctx, double *dispatch_ms, int64_t *n_dispatch,
                                   double *update_ms, int64_t *n_update) {
   if (!ctx) return fail(MOE_ERR_INVALID, "moe_ctx_get_timing: NULL ctx");
-  double sums[4];
-  int64_t counts[4];
+  double sums[MOE_TIMING_STAGES];
+  int64_t counts[MOE_TIMING_STAGES];
   const int st = moe_ctx_get_timing_ex(ctx, sums, counts);
   if (st) return st;
-  if (dispatch_ms) *dispatch_ms = sums[0];
-  if (n_dispatch) *n_dispatch = counts[0];
-  if (update_ms) *update_ms = sums[1];
-  if (n_update) *n_update = counts[1];
+  if (dispatch_ms) *dispatch_ms = sums[MOE_T_DISPATCH];
+  if (n_dispatch) *n_dispatch = counts[MOE_T_DISPATCH];
+  if (update_ms) *update_ms = sums[MOE_T_STAGE];
+  if (n_update) *n_update = counts[MOE_T_STAGE];
   return MOE_OK;
 }
 

@@ -95,7 +95,7 @@ struct moe_ctx {
 
   // measurement hooks (moe_ctx_set_timing): event pairs per stage, recycled
   bool timing;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool, ev_disp, ev_upd, ev_presum, ev_repl;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool, ev_disp, ev_upd, ev_presum, ev_repl, ev_stage;
 };
 
 namespace moe {

@@ -608,10 +608,20 @@ __global__ void __launch_bounds__(kThreads) k_replicate(const __grid_constant__ 
   const uint16_t *src = a.w[v] + (int64_t)(j0 - h * a.S) * a.P;
   uint16_t *dst = a.w[v] + (int64_t)l * a.P;
   const int64_t nrem = a.P - a.Pg, own = (int64_t)h * a.Pg;  // remote owners' elements
-  for (int64_t r = ((int64_t)blockIdx.x * kThreads + threadIdx.x) * kVec; r < nrem;
-       r += (int64_t)gridDim.x * kThreads * kVec) {
-    const int64_t i = r < own ? r : r + a.Pg;
-    st_stream(dst + i, ld_stream(src + i));
+  constexpr int kU = 4;  // 16-byte vectors in flight per thread
+  const int64_t stride = (int64_t)gridDim.x * kThreads * kVec;
+  for (int64_t r0 = ((int64_t)blockIdx.x * kThreads + threadIdx.x) * kVec; r0 < nrem; r0 += kU * stride) {
+    uint4 buf[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t r = r0 + u * stride;
+      if (r < nrem) buf[u] = ld_stream(src + (r < own ? r : r + a.Pg));
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t r = r0 + u * stride;
+      if (r < nrem) st_stream(dst + (r < own ? r : r + a.Pg), buf[u]);
+    }
   }
 }
 
@@ -797,7 +807,7 @@ int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *pl
   } else {
     const int64_t grid = std::min<int64_t>(items, (int64_t)ctx->num_sms * 2);
     if (grid > 0) {
-      const auto tev = dedup ? std::pair<cudaEvent_t, cudaEvent_t>{nullptr, nullptr} : timing_begin(ctx, s);
+      const auto tev = timing_begin(ctx, s);
       k_update_tma<<<(unsigned)grid, kTmaThreads, kTmaSmem, s>>>(a);
       MOE_CUDA_TRY(cudaGetLastError());
       timing_end(ctx->ev_upd, tev, s);
@@ -827,13 +837,13 @@ int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *pl
     }
     if (ndup > 0) {
       const int gx = std::max(1, std::min<int>((int)((ctx->P - ctx->Pg) / (kThreads * kVec)) + 1,
-                                               4 * ctx->num_sms / ndup + 1));
+                                               8 * ctx->num_sms / ndup + 1));
       const auto rev = timing_begin(ctx, s);
       k_replicate<<<dim3(gx, ctx->n_local * ctx->S), kThreads, 0, s>>>(ra);
       MOE_CUDA_TRY(cudaGetLastError());
       timing_end(ctx->ev_repl, rev, s);
     }
-    timing_end(ctx->ev_upd, stage_ev, s);
+    timing_end(ctx->ev_stage, stage_ev, s);
   }
   return MOE_OK;
 }
