@@ -134,8 +134,8 @@ def update_stage_bytes(fs_cur, fs_next, G: int, S: int, P: int, E: int, dedup: b
                 if g != h:
                     nout[g] += 2 * Pg * n
                     nin[h] += 2 * Pg * n
-            if dedup and r > 1:
-                rep[h] += (r - 1) * 2 * 2 * (P - Pg)
+            if dedup and r > 1:  # read the first slot's remote ranges once, write r - 1 copies
+                rep[h] += 2 * (P - Pg) + (r - 1) * 2 * (P - Pg)
     hbm = max(u + p + q for u, p, q in zip(upd, pre, rep))
     nvl = max(max(nin), max(nout))
     if parts:
