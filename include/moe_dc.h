@@ -50,7 +50,7 @@
 extern "C" {
 #endif
 
-#define MOE_ABI_VERSION 2
+#define MOE_ABI_VERSION 3
 #define MOE_MAX_E 256     /* experts per layer                              */
 #define MOE_MAX_G 8       /* GPUs: one NVSwitch box                         */
 #define MOE_MAX_SLOTS 4096 /* G*S                                           */
@@ -92,8 +92,13 @@ typedef struct {
 
 typedef enum {
   MOE_PLAN_PAPER_ALG1 = 0, /* Alg. 1 exactly (readings A2-A5) */
-  MOE_PLAN_MINMAX = 1      /* greedy Adams apportionment: minimises max C_e / r_e
+  MOE_PLAN_MINMAX = 1,     /* greedy Adams apportionment: minimises max C_e / r_e
                               (reading A1)                                        */
+  MOE_PLAN_STATIC = 2,     /* row f2, reading B2: the static baseline's uniform replication,
+                              r_e = G*S/E (remainder to the lowest indices); counts ignored
+                              ("an equal number of expert instances")          */
+  MOE_PLAN_KEEP = 3        /* moe_step only (row f2, reading B3 interval policy): plan_next =
+                              plan_cur, i.e. no re-placement this iteration                  */
 } moe_plan_policy;
 
 /* counts: [E] global pair counts C_e >= 0 (host).  sum == 0 means uniform (reading A3).
@@ -101,6 +106,11 @@ typedef enum {
  * Errors: MOE_ERR_INVALID (E<1, G<1, slots<1, E>G*slots, E>MOE_MAX_E,
  * G*slots>MOE_MAX_SLOTS, a NULL pointer, a negative count).                      */
 int moe_plan(const int64_t *counts, int32_t E, int32_t G, int32_t slots, moe_plan_t *out);
+
+/* Row f2: slot capacity for a capacity factor (capacity_factor x
+ * tokens / (s N) per slot): max(1, floor(cf * T * k / (G * S))), T global tokens
+ * (tokens counted as (token, expert) pairs, reading A6).  Returns -1 on invalid input.      */
+int32_t moe_slot_capacity(double cf, int64_t T, int32_t k, int32_t G, int32_t S);
 
 /* As moe_plan with an explicit policy.  steps (nullable, [2]) receives the number of
  * over- and under-allocation correction steps of Alg. 1 (0 for MINMAX).           */
@@ -207,6 +217,13 @@ typedef struct {
   int64_t *counts_dev;  /* [E] C_e (device, nullable)                                      */
   int64_t *counts_host; /* [E] C_e (PINNED host, nullable): input of the next moe_plan;
                            valid once the stream work enqueued by this call completes      */
+  /* Row f2 (capacity and drops; reading B1).
+   * capacity (INPUT): per-replica slot capacity; 0 = unlimited (the drop-free hot path).
+   * With capacity > 0 every replica keeps its pairs with offset < capacity (the highest
+   * offsets are dropped): dropped pairs get dest_slot = dest_off = -1 and are not in
+   * send_pair/send_gate; send_count and slot_load count kept pairs only.                   */
+  int32_t capacity;
+  int64_t *drops;       /* [E] dropped pairs per expert (device, nullable)                  */
 } moe_dispatch_out;
 
 int moe_dispatch(moe_ctx *ctx, const int32_t *topk_ids, const float *gates, int64_t T,

@@ -24,7 +24,14 @@ Per-rank outputs (rank g's local pair index p = t*k + j):
   dest_slot[p], dest_off[p]   -- where the pair goes
   send_pair / send_gate      -- local pairs ordered by (slot, off) (slot-major)
   send_count[j]              -- local pairs going to global slot j
-Reading A9: drop-free (no capacity), so every pair is placed.
+Reading A9: the hot path is drop-free (no capacity), so every pair is placed.
+
+Row f2 (capacity and drops; PAPER.md:885-900 sec:design_sched), reading B1:
+with a slot capacity `cap`, every replica keeps the pairs with offset < cap and drops the rest
+(the highest offsets first); dropped pairs get dest_slot = dest_off = -1 and are not sent;
+slot_load is the kept load min(load, cap); drops[e] = sum over e's replicas of
+max(0, load - cap).  slot_capacity(cf) = max(1, floor(cf * T * k / (G*S))) for T global tokens
+(SPEC.md:200 with tokens counted as pairs, reading A6).
 """
 from __future__ import annotations
 
@@ -50,8 +57,15 @@ def counts(ids_per_rank, E: int) -> np.ndarray:
     return out
 
 
-def dispatch(ids_per_rank, gates_per_rank, first_slot, E: int) -> dict:
-    """Replica-balanced dispatch of all ranks' pairs under a contiguous plan."""
+def slot_capacity(cf: float, T_global: int, k: int, GS: int) -> int:
+    """max(1, floor(cf * tokens / (s N))), tokens = pairs (reading A6)."""
+    return max(1, int(np.floor(cf * T_global * k / GS)))
+
+
+def dispatch(ids_per_rank, gates_per_rank, first_slot, E: int, capacity: int = 0) -> dict:
+    """Replica-balanced dispatch of all ranks' pairs under a contiguous plan.
+
+    capacity > 0: per-replica capacity (row f2); 0: unlimited (the drop-free hot path)."""
     G = len(ids_per_rank)
     for ids in ids_per_rank:
         validate_ids(np.asarray(ids), E)
@@ -79,25 +93,36 @@ def dispatch(ids_per_rank, gates_per_rank, first_slot, E: int) -> dict:
     off = R - (rho * qe + np.minimum(rho, me))
     slot = fs[glob] + rho
 
-    slot_load = np.zeros(GS, dtype=np.int64)
+    load = np.zeros(GS, dtype=np.int64)
     for e in range(E):
         for p in range(int(r[e])):
-            slot_load[fs[e] + p] = q[e] + (1 if p < m[e] else 0)
+            load[fs[e] + p] = q[e] + (1 if p < m[e] else 0)
+    if capacity > 0:  # row f2: keep offsets < capacity in every replica
+        kept = off < capacity
+        slot_load = np.minimum(load, capacity)
+        drops = np.array([int((load[fs[e]:fs[e + 1]] - slot_load[fs[e]:fs[e + 1]]).sum())
+                          for e in range(E)], dtype=np.int64)
+    else:
+        kept = np.ones(glob.size, dtype=bool)
+        slot_load = load
+        drops = np.zeros(E, dtype=np.int64)
 
-    out = {"cnt": cnt, "C": C, "slot_load": slot_load, "ranks": []}
+    out = {"cnt": cnt, "C": C, "slot_load": slot_load, "drops": drops, "ranks": []}
     base = 0
     for g in range(G):
         n = flat[g].size
-        ds = slot[base:base + n]
-        do = off[base:base + n]
-        order = np.lexsort((do, ds))            # by slot, then offset
+        kp = kept[base:base + n]
+        ds = np.where(kp, slot[base:base + n], -1)
+        do = np.where(kp, off[base:base + n], -1)
+        idx = np.nonzero(kp)[0]
+        order = idx[np.lexsort((do[idx], ds[idx]))]   # kept pairs by slot, then offset
         gates = np.asarray(gates_per_rank[g], dtype=np.float32).reshape(-1)
         out["ranks"].append({
             "dest_slot": ds.astype(np.int32),
             "dest_off": do.astype(np.int32),
             "send_pair": order.astype(np.int32),
             "send_gate": gates[order],
-            "send_count": np.bincount(ds, minlength=GS).astype(np.int32),
+            "send_count": np.bincount(ds[idx], minlength=GS).astype(np.int32),
         })
         base += n
     return out

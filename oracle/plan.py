@@ -87,6 +87,14 @@ def minmax(counts, E: int, G: int, S: int) -> np.ndarray:
     return np.array(r, dtype=np.int64)
 
 
+def static(E: int, G: int, S: int) -> np.ndarray:
+    """Reading B2 (row f2): the static baseline's uniform replication r = sN/E (PAPER.md:1014,
+    "an equal number of expert instances"), remainder to the lowest indices; ignores counts."""
+    _validate(np.zeros(E, dtype=np.int64), E, G, S)
+    GS = G * S
+    return np.array([GS // E + (1 if e < GS % E else 0) for e in range(E)], dtype=np.int64)
+
+
 def placement(replicas) -> tuple[np.ndarray, np.ndarray]:
     """Contiguous map: first_slot [E+1], slot_expert [sum r]."""
     r = np.asarray(replicas, dtype=np.int64)
@@ -96,7 +104,15 @@ def placement(replicas) -> tuple[np.ndarray, np.ndarray]:
 
 
 def plan(counts, E: int, G: int, S: int, policy: str = "alg1") -> dict:
-    r = alg1(counts, E, G, S) if policy == "alg1" else minmax(counts, E, G, S)
+    if policy == "alg1":
+        r = alg1(counts, E, G, S)
+    elif policy == "minmax":
+        r = minmax(counts, E, G, S)
+    elif policy == "static":
+        _validate(counts, E, G, S)
+        r = static(E, G, S)
+    else:
+        raise ValueError(f"unknown policy {policy}")
     fs, se = placement(r)
     return {"E": E, "G": G, "S": S, "replicas": r, "first_slot": fs, "slot_expert": se}
 

@@ -63,10 +63,15 @@ class OracleSim:
 
     def __init__(self, E: int, G: int, S: int, P: int, seed_master: int,
                  hyper: _adam.AdamHyper = _adam.AdamHyper(), policy: str = "alg1",
-                 scale_mode: int = 0, scale=None, idx=None, master0=None):
+                 scale_mode: int = 0, scale=None, idx=None, master0=None,
+                 capacity: int = 0, replan_interval: int = 1):
+        """capacity > 0 and replan_interval > 1 are row f2 (readings B1, B3): per-replica
+        capacity with drops, and a placement recomputed only every `replan_interval`
+        iterations (from the latest counts) instead of every iteration."""
         from synth import hashgen  # input generator only (no method arithmetic)
         self.E, self.G, self.S, self.P = E, G, S, P
         self.hyper, self.policy = hyper, policy
+        self.capacity, self.replan_interval = capacity, replan_interval
         self.scale_mode, self.scale = scale_mode, scale
         self.idx = np.arange(P, dtype=np.int64) if idx is None else np.asarray(idx, dtype=np.int64)
         if master0 is None:
@@ -83,8 +88,12 @@ class OracleSim:
         """grad_of_slot(j) -> uint16 bf16 bits of global slot j's grad over ``idx``."""
         E, G, S = self.E, self.G, self.S
         plan_t = self.plan
-        disp = _dispatch.dispatch(ids_per_rank, gates_per_rank, plan_t["first_slot"], E)   # a0, a2
-        plan_next = _plan.plan(disp["C"], E, G, S, self.policy)                            # a1
+        disp = _dispatch.dispatch(ids_per_rank, gates_per_rank, plan_t["first_slot"], E,
+                                  self.capacity)                                            # a0, a2
+        if self.step % self.replan_interval == 0:
+            plan_next = _plan.plan(disp["C"], E, G, S, self.policy)                        # a1
+        else:  # interval policy (reading B3): keep the placement until the next re-plan
+            plan_next = plan_t
         sc = _adam.scalars(self.hyper, self.step)
         for e in range(E):
             g = reduce_expert(grad_of_slot, plan_t["first_slot"], e, S,
@@ -104,7 +113,8 @@ class OracleSim:
         assert int(r.sum()) == self.G * self.S, "replicas fill exactly G*S slots"
         assert (np.diff(plan_next["slot_expert"]) >= 0).all(), "contiguous placement"
         pairs = sum(int(np.asarray(i).size) for i in ids_per_rank)
-        assert int(disp["slot_load"].sum()) == int(disp["C"].sum()) == pairs, "conservation"
+        assert int(disp["C"].sum()) == pairs
+        assert int(disp["slot_load"].sum()) + int(disp["drops"].sum()) == pairs, "conservation"
         fs = self.plan["first_slot"]
         for e in range(self.E):
             ld = disp["slot_load"][fs[e]:fs[e + 1]]

@@ -7,6 +7,7 @@ one MoE layer's iteration.  There is no CPU fallback: importing ``api`` without 
 library raises.
 """
 from .api import (AdamConfig, DispatchBuffers, MoeContext, MoeError, Plan,  # noqa: F401
-                  MOE_PLAN_MINMAX, MOE_PLAN_PAPER_ALG1, moe_dispatch, moe_place, moe_plan,
-                  moe_step, moe_update, synth_grads, synth_master)
+                  MOE_OPT_DEDUP, MOE_PLAN_KEEP, MOE_PLAN_MINMAX, MOE_PLAN_PAPER_ALG1,
+                  MOE_PLAN_STATIC, moe_dispatch, moe_place, moe_plan, moe_slot_capacity, moe_step,
+                  moe_update, synth_grads, synth_master)
 from .layer import DecoupledExpertLayer  # noqa: F401

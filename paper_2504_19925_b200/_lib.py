@@ -15,11 +15,12 @@ MOE_OK = 0
 STATUS = {0: "MOE_OK", 1: "MOE_ERR_INVALID", 2: "MOE_ERR_SHAPE", 3: "MOE_ERR_DATA",
           4: "MOE_ERR_CUDA", 5: "MOE_ERR_COMM", 6: "MOE_ERR_INTERNAL", 7: "MOE_ERR_TIMEOUT"}
 MOE_MAX_E, MOE_MAX_G, MOE_MAX_SLOTS = 256, 8, 4096
-MOE_PLAN_PAPER_ALG1, MOE_PLAN_MINMAX = 0, 1
+MOE_PLAN_PAPER_ALG1, MOE_PLAN_MINMAX, MOE_PLAN_STATIC, MOE_PLAN_KEEP = 0, 1, 2, 3
 
 # every symbol include/*.h declares (checked by tests/test_abi.py)
 EXPORTED = [
     "moe_status_str", "moe_last_error", "moe_abi_version", "moe_plan", "moe_plan_ex",
+    "moe_slot_capacity",
     "moe_ctx_create", "moe_ctx_destroy", "moe_ctx_handle_bytes", "moe_ctx_export",
     "moe_ctx_connect", "moe_ctx_check", "moe_ctx_wait_counts", "moe_dispatch", "moe_update",
     "moe_place", "moe_step", "moe_ctx_set_timing", "moe_ctx_get_timing", "moe_ctx_get_timing_ex",
@@ -51,7 +52,8 @@ MOE_OPT_DEDUP = 1
 class MoeDispatchOut(C.Structure):
     _fields_ = [("dest_slot", C.c_void_p), ("dest_off", C.c_void_p), ("send_pair", C.c_void_p),
                 ("send_gate", C.c_void_p), ("send_count", C.c_void_p), ("slot_load", C.c_void_p),
-                ("counts_dev", C.c_void_p), ("counts_host", C.c_void_p)]
+                ("counts_dev", C.c_void_p), ("counts_host", C.c_void_p),
+                ("capacity", C.c_int32), ("drops", C.c_void_p)]
 
 
 class MoeAdamT(C.Structure):
@@ -75,6 +77,8 @@ def lib() -> C.CDLL:
         L.moe_last_error.restype = C.c_char_p
         L.moe_last_error.argtypes = []
         L.moe_abi_version.restype = C.c_int
+        L.moe_slot_capacity.restype = C.c_int32
+        L.moe_slot_capacity.argtypes = [C.c_double, C.c_int64, C.c_int32, C.c_int32, C.c_int32]
         L.moe_plan.restype = C.c_int
         L.moe_plan.argtypes = [_i64p, C.c_int32, C.c_int32, C.c_int32, C.POINTER(MoePlanT)]
         L.moe_plan_ex.restype = C.c_int

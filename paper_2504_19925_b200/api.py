@@ -13,7 +13,8 @@ import numpy as np
 import torch
 
 from . import _lib as L
-from ._lib import MOE_OPT_DEDUP, MOE_PLAN_MINMAX, MOE_PLAN_PAPER_ALG1, MoeError, check  # noqa: F401
+from ._lib import (MOE_OPT_DEDUP, MOE_PLAN_KEEP, MOE_PLAN_MINMAX, MOE_PLAN_PAPER_ALG1,  # noqa: F401
+                   MOE_PLAN_STATIC, MoeError, check)
 
 
 def _stream_ptr(stream) -> C.c_void_p:
@@ -51,6 +52,14 @@ class Plan:
         p.replicas[:] = np.diff(fs)
         p.slot_expert[:] = np.repeat(np.arange(p.E, dtype=np.int32), p.replicas)
         return p
+
+
+def moe_slot_capacity(cf: float, T: int, k: int, G: int, S: int) -> int:
+    """Row f2: max(1, floor(cf * T * k / (G * S))) (computed by the C library)."""
+    c = L.lib().moe_slot_capacity(cf, T, k, G, S)
+    if c < 0:
+        raise ValueError("moe_slot_capacity: invalid arguments")
+    return int(c)
 
 
 def moe_plan(counts, E: int, G: int, slots: int, policy: int = MOE_PLAN_PAPER_ALG1,
@@ -174,7 +183,7 @@ class MoeContext:
 class DispatchBuffers:
     """Caller-owned outputs of moe_dispatch (moe_dispatch_out)."""
 
-    def __init__(self, ctx: MoeContext, T: int, pinned_counts: bool = True):
+    def __init__(self, ctx: MoeContext, T: int, pinned_counts: bool = True, capacity: int = 0):
         dev = torch.device("cuda", ctx.device)
         n = ctx.n_local * T * ctx.k
         GS = ctx.G * ctx.S
@@ -187,9 +196,18 @@ class DispatchBuffers:
         self.slot_load = torch.empty(GS, dtype=torch.int32, device=dev)
         self.counts_dev = torch.empty(ctx.E, dtype=torch.int64, device=dev)
         self.counts_host = torch.zeros(ctx.E, dtype=torch.int64, pin_memory=pinned_counts)
+        self.drops = torch.zeros(ctx.E, dtype=torch.int64, device=dev)
         self._c = L.MoeDispatchOut(*(t.data_ptr() for t in (
             self.dest_slot, self.dest_off, self.send_pair, self.send_gate, self.send_count,
-            self.slot_load, self.counts_dev, self.counts_host)))
+            self.slot_load, self.counts_dev, self.counts_host)), 0, self.drops.data_ptr())
+        self.set_capacity(capacity)
+
+    def set_capacity(self, capacity: int) -> None:
+        """Row f2: per-replica capacity for the next dispatches (0 = unlimited, drop-free)."""
+        if capacity < 0:
+            raise ValueError("capacity must be >= 0")
+        self._c.capacity = int(capacity)
+        self.capacity = int(capacity)
 
     @property
     def c(self) -> L.MoeDispatchOut:

@@ -72,6 +72,7 @@ void free_ctx(moe_ctx *c) {
   cudaFree(c->done);
   cudaFree(c->blk);
   cudaFree(c->einfo);
+  cudaFree(c->kept_pre);
   cudaFree(c->counts_dev);
   cudaFree(c->err);
   cudaFree(c->item_ctr);
@@ -134,6 +135,7 @@ extern "C" int moe_ctx_create(const moe_ctx_desc *d, moe_ctx **out) {
   c->done = nullptr;
   c->blk = nullptr;
   c->einfo = nullptr;
+  c->kept_pre = nullptr;
   c->counts_dev = nullptr;
   c->err = nullptr;
   c->item_ctr = nullptr;
@@ -160,6 +162,7 @@ extern "C" int moe_ctx_create(const moe_ctx_desc *d, moe_ctx **out) {
   chk(cudaMalloc(&c->done, sizeof(uint32_t) * n_local));
   chk(cudaMalloc(&c->blk, sizeof(int32_t) * n_local * c->E * c->nb_max));
   chk(cudaMalloc(&c->einfo, sizeof(ExpertInfo) * n_local * c->E));
+  chk(cudaMalloc(&c->kept_pre, sizeof(int32_t) * n_local * c->G * c->S));
   chk(cudaMalloc(&c->counts_dev, sizeof(int64_t) * c->E));
   chk(cudaMalloc(&c->err, sizeof(int32_t)));
   chk(cudaMalloc(&c->item_ctr, 3 * sizeof(unsigned long long)));

@@ -120,8 +120,33 @@ struct ScanArgs {
   uint32_t *scan_done;   // block counter (self-resetting)
   uint32_t *host_flag;   // pinned host word: set to `epoch` once counts_host is complete
   int32_t *err;
+  int32_t cap;           // per-replica capacity (row f2), 0 = unlimited
+  int64_t *drops;        // [E] dropped pairs (nullable)
+  int32_t *kept_pre;     // [n_local][G*S]
   int32_t fs[MOE_MAX_E + 1];
 };
+
+// Block-wide exclusive scan of one int per thread (kThreads threads); returns the exclusive
+// prefix and writes the block total to *total.  Uses `wsum` (kThreads/32 ints of smem).
+__device__ __forceinline__ int32_t block_exclusive_scan(int32_t val, int32_t *wsum, int32_t *total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int32_t incl = val;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += y;
+  }
+  __syncthreads();  // wsum may still be read by a previous call
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  int32_t woff = 0, tot = 0;
+  for (int w = 0; w < kThreads / 32; ++w) {
+    if (w < warp) woff += wsum[w];
+    tot += wsum[w];
+  }
+  *total = tot;
+  return woff + incl - val;
+}
 
 __device__ __forceinline__ int32_t ld_cg(const int32_t *p) { return __ldcg(p); }
 
@@ -135,7 +160,7 @@ __global__ void __launch_bounds__(kThreads) k_scan(const __grid_constant__ ScanA
   const int v = blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int grank = a.real ? a.rank : v;
-  __shared__ int32_t s_base, s_cnt, s_C, s_loc;
+  __shared__ int32_t s_base, s_cnt, s_C;
   __shared__ int32_t wsum[kThreads / 32];
   __shared__ int ok;
   pdl_trigger();
@@ -149,42 +174,59 @@ __global__ void __launch_bounds__(kThreads) k_scan(const __grid_constant__ ScanA
   }
   __syncthreads();
   if (!ok) return;
-  if (warp == 0) {  // warp-parallel: C_e and this rank's base (over GPUs), loc_off (over experts)
+  if (warp == 0) {  // warp-parallel: C_e and this rank's base over GPUs
     const int32_t(*x)[MOE_MAX_E] = a.sync->xcnt[a.parity];
     const int32_t c = lane < a.G ? ld_cg(&x[lane][e]) : 0;
-    int32_t C = c, base = lane < grank ? c : 0, loc = 0;
-    for (int e2 = lane; e2 < e; e2 += 32) loc += ld_cg(&x[grank][e2]);
+    int32_t C = c, base = lane < grank ? c : 0;
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
       C += __shfl_xor_sync(0xffffffffu, C, d);
       base += __shfl_xor_sync(0xffffffffu, base, d);
-      loc += __shfl_xor_sync(0xffffffffu, loc, d);
     }
     if (lane == 0) {
       s_base = base;
       s_cnt = ld_cg(&x[grank][e]);
       s_C = C;
-      s_loc = loc;
     }
   }
   __syncthreads();
   const int32_t C = s_C, base = s_base, cnt = s_cnt;
   const int32_t f0 = a.fs[e], r = a.fs[e + 1] - f0;
   const int32_t q = C / r, m = C % r;
+  const int32_t capv = a.cap > 0 ? a.cap : 0x7fffffff;
   const int GS = a.G * a.S;
-  if (v == 0) {
-    if (tid == 0) {
-      a.counts_dev[e] = C;
-      if (a.counts_host) a.counts_host[e] = C;  // straight to pinned host memory (PCIe write)
+  if (v == 0 && tid == 0) {
+    a.counts_dev[e] = C;
+    if (a.counts_host) a.counts_host[e] = C;  // straight to pinned host memory (PCIe write)
+  }
+  // Per replica rho: load q or q+1, kept min(load, cap) (row f2), this rank's kept pairs in it
+  // (send_count) and their exclusive prefix over rho (kept_pre: where the replica's kept pairs
+  // start in this rank's slot-major order of e).
+  int32_t carry = 0, dropped = 0;
+  for (int r0 = 0; r0 < r; r0 += kThreads) {
+    const int rho = r0 + tid;
+    int32_t mine = 0;
+    if (rho < r) {
+      const int32_t start = rho * q + min(rho, m), load = q + (rho < m ? 1 : 0);
+      const int32_t kept = min(load, capv);
+      const int32_t lo = max(base, start), hi = min(base + cnt, start + kept);
+      mine = max(0, hi - lo);
+      dropped += load - kept;
+      if (v == 0) a.slot_load[f0 + rho] = kept;
+      a.send_count[(int64_t)v * GS + f0 + rho] = mine;
     }
-    for (int rho = tid; rho < r; rho += kThreads) a.slot_load[f0 + rho] = q + (rho < m ? 1 : 0);
+    int32_t tot;
+    const int32_t excl = block_exclusive_scan(mine, wsum, &tot);
+    if (rho < r) a.kept_pre[(int64_t)v * GS + f0 + rho] = carry + excl;
+    carry += tot;
   }
-  for (int rho = tid; rho < r; rho += kThreads) {
-    const int32_t start = rho * q + min(rho, m), len = q + (rho < m ? 1 : 0);
-    const int32_t lo = max(base, start), hi = min(base + cnt, start + len);
-    a.send_count[(int64_t)v * GS + f0 + rho] = max(0, hi - lo);
+  if (v == 0 && a.drops) {
+    int32_t dtot;
+    block_exclusive_scan(dropped, wsum, &dtot);
+    if (tid == 0) a.drops[e] = dtot;
   }
-  if (tid == 0) a.einfo[v * a.E + e] = ExpertInfo{base, s_loc, q, m};
+  if (tid == 0) a.einfo[v * a.E + e] = ExpertInfo{base, carry, q, m};
+  __syncthreads();  // wsum is reused by the tile scan below
 
   // exclusive scan of this rank's tile counts of expert e, in place
   int32_t *row = a.blk + ((int64_t)v * a.E + e) * a.nb_max;
@@ -226,9 +268,10 @@ struct ScatterArgs {
   const int32_t *ids;
   const float *gates;
   int64_t npairs;
-  int32_t E, nb, nb_max, tile;
+  int32_t E, nb, nb_max, tile, GS, cap;
   const int32_t *blk;
   const ExpertInfo *einfo;
+  const int32_t *kept_pre;  // [n_local][G*S]
   int32_t *dest_slot, *dest_off, *send_pair;
   float *send_gate;
   int32_t fs[MOE_MAX_E + 1];
@@ -239,6 +282,7 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ Sc
   __shared__ int32_t wcnt[kWarps][MOE_MAX_E];
   __shared__ ExpertInfo s_info[MOE_MAX_E];
   __shared__ int32_t s_blk[MOE_MAX_E];
+  __shared__ int32_t s_loc[MOE_MAX_E];  // where expert e's kept pairs start in this rank's send order
   extern __shared__ int32_t s_tile[];  // [tile] ids, then [tile] gates (bit patterns)
   const int v = blockIdx.x / a.nb;
   const int b = blockIdx.x % a.nb;
@@ -260,6 +304,32 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ Sc
     for (int w = 0; w < kWarps; ++w) wcnt[w][e] = 0;
   }
   __syncthreads();
+  if (warp == 0) {  // s_loc = exclusive prefix over experts of this rank's kept counts
+    constexpr int kPer = MOE_MAX_E / 32;
+    int32_t c[kPer], s = 0;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const int e = lane * kPer + i;
+      c[i] = e < a.E ? s_info[e].kcnt : 0;
+      s += c[i];
+    }
+    int32_t incl = s;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += y;
+    }
+    int32_t run = incl - s;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const int e = lane * kPer + i;
+      if (e < a.E) s_loc[e] = run;
+      run += c[i];
+    }
+  }
+  __syncthreads();
+  const int32_t capv = a.cap > 0 ? a.cap : 0x7fffffff;
+  const int32_t *kept_pre = a.kept_pre + (int64_t)v * a.GS;
 
   // Warp w owns the consecutive pairs [w*R*32, (w+1)*R*32) of the tile (R = tile/256 rounds of
   // 32): pair order == (warp, round, lane) order, so the ranks below are stable.
@@ -320,10 +390,20 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ Sc
     const int32_t q = info.q, m = info.m;
     const int32_t big = m * (q + 1);
     const int32_t rho = R < big ? R / (q + 1) : m + (R - big) / q;
-    const int32_t off = R - (rho * q + min(rho, m));
-    a.dest_slot[off_v + p] = a.fs[e] + rho;
+    const int32_t start = rho * q + min(rho, m);
+    const int32_t off = R - start;
+    if (off >= capv) {  // row f2: beyond the replica's capacity -> dropped, not sent
+      a.dest_slot[off_v + p] = -1;
+      a.dest_off[off_v + p] = -1;
+      continue;
+    }
+    const int32_t slot = a.fs[e] + rho;
+    a.dest_slot[off_v + p] = slot;
     a.dest_off[off_v + p] = off;
-    const int64_t pos = off_v + info.loc_off + lr;
+    // slot-major position among this rank's kept pairs: experts before e, kept pairs of this
+    // rank in e's earlier replicas, then this rank's pairs in replica rho before this one
+    // (all kept: a replica keeps a prefix of its offsets)
+    const int64_t pos = off_v + s_loc[e] + kept_pre[slot] + (R - max(info.base, start));
     a.send_pair[pos] = (int32_t)p;
     a.send_gate[pos] = __int_as_float(s_tile[a.tile + (p - tbase)]);
   }
@@ -366,6 +446,7 @@ extern "C" int moe_dispatch(moe_ctx *ctx, const int32_t *topk_ids, const float *
                  !out->send_gate)) ||
       !out->send_count || !out->slot_load)
     return fail(MOE_ERR_INVALID, "moe_dispatch: NULL buffer");
+  if (out->capacity < 0) return fail(MOE_ERR_INVALID, "moe_dispatch: capacity must be >= 0");
   if (ctx->rank >= 0 && ctx->G > 1 && !ctx->connected)
     return fail(MOE_ERR_INVALID, "moe_dispatch: real-mode context not connected");
   int st = moe_validate_plan(ctx, plan, "moe_dispatch");
@@ -435,6 +516,9 @@ extern "C" int moe_dispatch(moe_ctx *ctx, const int32_t *topk_ids, const float *
   sa.scan_done = ctx->scan_done;
   sa.host_flag = ctx->host_flag_dev;
   sa.err = ctx->err;
+  sa.cap = out->capacity;
+  sa.drops = out->drops;
+  sa.kept_pre = ctx->kept_pre;
   for (int e = 0; e <= ctx->E; ++e) sa.fs[e] = plan->first_slot[e];
   MOE_CUDA_TRY(launch_pdl(k_scan, dim3(ctx->E, ctx->n_local), s, sa));
   ctx->counts_pending = true;
@@ -453,6 +537,9 @@ extern "C" int moe_dispatch(moe_ctx *ctx, const int32_t *topk_ids, const float *
   ca.dest_off = out->dest_off;
   ca.send_pair = out->send_pair;
   ca.send_gate = out->send_gate;
+  ca.GS = ctx->G * ctx->S;
+  ca.cap = out->capacity;
+  ca.kept_pre = ctx->kept_pre;
   for (int e = 0; e <= ctx->E; ++e) ca.fs[e] = plan->first_slot[e];
   if (npairs > 0)
     MOE_CUDA_TRY(launch_pdl(k_scatter, dim3(nb * ctx->n_local), s, ca, (size_t)2 * tile * sizeof(int32_t)));

@@ -36,7 +36,7 @@ struct SyncBuf {
 // Per-expert dispatch parameters computed by the scan kernel, read by the scatter kernel.
 struct ExpertInfo {
   int32_t base;     // global rank of this rank's first pair of the expert
-  int32_t loc_off;  // offset of the expert's first pair in this rank's slot-major order
+  int32_t kcnt;     // this rank's kept pairs of the expert (all of them without capacity)
   int32_t q, m;     // C_e / r_e, C_e % r_e
 };
 
@@ -82,6 +82,7 @@ struct moe_ctx {
   uint32_t *done;           // [n_local] last-block tickets of the histogram kernel
   int32_t *blk;             // [n_local][E][nb_max] block counts, scanned in place
   moe::ExpertInfo *einfo;   // [n_local][E]
+  int32_t *kept_pre;        // [n_local][G*S] this rank's kept pairs in earlier replicas of the slot's expert
   int64_t *counts_dev;      // [E]
   int32_t *err;             // device error bits
   unsigned long long *item_ctr;  // [3] counters of k_update_tma (self-resetting)

@@ -123,12 +123,17 @@ extern "C" int moe_plan_ex(const int64_t *counts, int32_t E, int32_t G, int32_t 
                            moe_plan_t *out, int64_t *steps) {
   int st = validate(counts, E, G, slots, out);
   if (st) return st;
-  if (policy == MOE_PLAN_PAPER_ALG1)
+  if (policy == MOE_PLAN_PAPER_ALG1) {
     alg1(counts, E, G, slots, out->replicas, steps);
-  else if (policy == MOE_PLAN_MINMAX)
+  } else if (policy == MOE_PLAN_MINMAX) {
     minmax(counts, E, G, slots, out->replicas, steps);
-  else
+  } else if (policy == MOE_PLAN_STATIC) {  // reading B2: uniform, remainder to the lowest indices
+    const int32_t GS = G * slots;
+    for (int e = 0; e < E; ++e) out->replicas[e] = GS / E + (e < GS % E ? 1 : 0);
+    if (steps) steps[0] = steps[1] = 0;
+  } else {
     return moe::fail(MOE_ERR_INVALID, "moe_plan: unknown policy %d", policy);
+  }
   // contiguous slot map
   int32_t j = 0;
   for (int e = 0; e < E; ++e) {
@@ -141,6 +146,13 @@ extern "C" int moe_plan_ex(const int64_t *counts, int32_t E, int32_t G, int32_t 
   out->S = slots;
   if (j != G * slots) return moe::fail(MOE_ERR_INTERNAL, "moe_plan: replicas sum %d != G*S", j);
   return MOE_OK;
+}
+
+extern "C" int32_t moe_slot_capacity(double cf, int64_t T, int32_t k, int32_t G, int32_t S) {
+  if (!(cf > 0.0) || T < 0 || k < 1 || G < 1 || S < 1) return -1;
+  const double c = std::floor(cf * (double)T * (double)k / ((double)G * (double)S));
+  if (c >= 2147483647.0) return 2147483647;
+  return c < 1.0 ? 1 : (int32_t)c;
 }
 
 extern "C" int moe_plan(const int64_t *counts, int32_t E, int32_t G, int32_t slots, moe_plan_t *out) {

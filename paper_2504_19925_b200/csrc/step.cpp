@@ -17,8 +17,21 @@ extern "C" int moe_step(moe_ctx *ctx, const int32_t *topk_ids, const float *gate
   if (st) return st;
   st = moe_ctx_wait_counts(ctx);  // C_t on the host
   if (st) return st;
-  st = moe_plan_ex(out->counts_host, plan_cur->E, plan_cur->G, plan_cur->S, policy, plan_next,
-                   nullptr);  // a1 -> plan_{t+1}
-  if (st) return st;
+  if (policy == MOE_PLAN_KEEP) {  // interval policy between re-plans: plan_{t+1} = plan_t
+    if (!plan_next->replicas || !plan_next->first_slot || !plan_next->slot_expert || !plan_cur->replicas ||
+        !plan_cur->slot_expert)
+      return moe::fail(MOE_ERR_INVALID, "moe_step: NULL plan array");
+    const int32_t E = plan_cur->E, GS = plan_cur->G * plan_cur->S;
+    for (int e = 0; e < E; ++e) plan_next->replicas[e] = plan_cur->replicas[e];
+    for (int e = 0; e <= E; ++e) plan_next->first_slot[e] = plan_cur->first_slot[e];
+    for (int j = 0; j < GS; ++j) plan_next->slot_expert[j] = plan_cur->slot_expert[j];
+    plan_next->E = E;
+    plan_next->G = plan_cur->G;
+    plan_next->S = plan_cur->S;
+  } else {
+    st = moe_plan_ex(out->counts_host, plan_cur->E, plan_cur->G, plan_cur->S, policy, plan_next,
+                     nullptr);  // a1 -> plan_{t+1}
+    if (st) return st;
+  }
   return moe_update(ctx, plan_cur, plan_next, adam, stream);  // a3 + a4 + a5
 }

@@ -23,7 +23,15 @@ class DecoupledExpertLayer:
     def __init__(self, E: int, G: int, S: int, k: int, P: int, max_tokens: int, rank: int = -1,
                  device: int | None = None, seed: int = 0, adam: api.AdamConfig | None = None,
                  policy: int = api.MOE_PLAN_PAPER_ALG1, scale_mode: int = 0, scale=None,
-                 init_master: bool = True, dedup: bool = False):
+                 init_master: bool = True, dedup: bool = False, capacity: int = 0,
+                 replan_interval: int = 1):
+        """capacity > 0 (per-replica slot capacity, see api.moe_slot_capacity) and
+        replan_interval > 1 (re-place only every i iterations; MOE_PLAN_STATIC for the static
+        baseline) are row f2 (readings B1-B3); the defaults are the paper's drop-free,
+        per-iteration path."""
+        if replan_interval < 1:
+            raise ValueError("replan_interval must be >= 1")
+        self.replan_interval = replan_interval
         if device is None:
             device = torch.cuda.current_device()
         self.E, self.G, self.S, self.k, self.P = E, G, S, k, P
@@ -45,7 +53,7 @@ class DecoupledExpertLayer:
                                   self.master, self.adam_m, self.adam_v, device=device,
                                   options=api.MOE_OPT_DEDUP if dedup else 0)
         self.dedup = dedup
-        self.out = api.DispatchBuffers(self.ctx, max_tokens)
+        self.out = api.DispatchBuffers(self.ctx, max_tokens, capacity=capacity)
         self.seed = seed
         if init_master:
             for v in range(n):
@@ -71,8 +79,14 @@ class DecoupledExpertLayer:
         api.moe_dispatch(self.ctx, topk_ids, gates, T, self.plan, self.out, stream)
         return self.out
 
+    def _replans(self) -> bool:
+        """Interval policy (reading B3): re-place after iterations t = i, 2i, ..."""
+        return self.t % self.replan_interval == 0
+
     def plan_next(self) -> api.Plan:
         self.ctx.wait_counts()
+        if not self._replans():
+            return api.Plan.from_first_slot(self.plan.first_slot, self.G, self.S)
         return api.moe_plan(self.out.counts_host.numpy(), self.E, self.G, self.S, self.policy)
 
     def update(self, plan_next: api.Plan, stream=None) -> None:
@@ -86,7 +100,8 @@ class DecoupledExpertLayer:
         dispatch -> host plan (overlapping the scatter kernel) -> reduce/Adam/place."""
         if not self._connected:
             raise RuntimeError("real-mode layer: call connect() first")
-        nxt = api.moe_step(self.ctx, topk_ids, gates, T, self.plan, self.policy, self.out, self.adam,
+        policy = self.policy if self._replans() else api.MOE_PLAN_KEEP
+        nxt = api.moe_step(self.ctx, topk_ids, gates, T, self.plan, policy, self.out, self.adam,
                            self.t, self.scale_mode, self.scale, stream)
         self.plan = nxt
         self.t += 1

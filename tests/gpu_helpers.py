@@ -16,7 +16,7 @@ def _u32(x: np.ndarray) -> np.ndarray:
 def run_parity(name: str, G: int, iters: int, *, rank_mode: str = "virtual", idx=None,
                T: int | None = None, policy: int = 0, scale_mode: int = 0, scale=None,
                weight_decay: float = 0.0, trace=None, check_dispatch: bool = True,
-               dedup: bool = False):
+               dedup: bool = False, capacity: int = 0, replan_interval: int = 1):
     """Returns the number of iterations compared.  rank_mode: "virtual" (rank=-1, G ranks on
     cuda:0) or "single" (real mode with G == 1)."""
     from paper_2504_19925_b200 import AdamConfig, DecoupledExpertLayer
@@ -36,11 +36,13 @@ def run_parity(name: str, G: int, iters: int, *, rank_mode: str = "virtual", idx
     adam = AdamConfig(lr=hyper.lr, beta1=hyper.beta1, beta2=hyper.beta2, eps=hyper.eps,
                       weight_decay=weight_decay)
     layer = DecoupledExpertLayer(E, G, S, k, P, Tg, rank=rank, device=0, seed=seed, adam=adam,
-                                 policy=policy, scale_mode=scale_mode, scale=scale, dedup=dedup)
-    pol = "alg1" if policy == 0 else "minmax"
+                                 policy=policy, scale_mode=scale_mode, scale=scale, dedup=dedup,
+                                 capacity=capacity, replan_interval=replan_interval)
+    pol = {0: "alg1", 1: "minmax", 2: "static"}[policy]
     idx_arr = np.arange(P, dtype=np.int64) if idx is None else np.asarray(idx, dtype=np.int64)
     sim = ostep.OracleSim(E, G, S, P, seed, hyper=hyper, policy=pol, scale_mode=scale_mode,
-                          scale=scale, idx=idx_arr)
+                          scale=scale, idx=idx_arr, capacity=capacity,
+                          replan_interval=replan_interval)
     idx_t = torch.from_numpy(idx_arr).cuda()
     Pg = P // G
     # initial placement (moe_place) equals the oracle's plan_0 placement
@@ -62,6 +64,8 @@ def run_parity(name: str, G: int, iters: int, *, rank_mode: str = "virtual", idx
         d = res["dispatch"]
         assert layer.out.counts_host.tolist() == d["C"].tolist(), f"iter {t}: counts"
         assert layer.out.slot_load.cpu().tolist() == d["slot_load"].tolist(), f"iter {t}: slot_load"
+        if capacity > 0:
+            assert layer.out.drops.cpu().tolist() == d["drops"].tolist(), f"iter {t}: drops"
         if check_dispatch:
             n = Tg * k
             ds = layer.out.dest_slot.cpu().numpy()
@@ -74,8 +78,9 @@ def run_parity(name: str, G: int, iters: int, *, rank_mode: str = "virtual", idx
                 sl = slice(v * n, (v + 1) * n)
                 assert np.array_equal(ds[sl], rk["dest_slot"]), f"iter {t} rank {v}: dest_slot"
                 assert np.array_equal(do[sl], rk["dest_off"]), f"iter {t} rank {v}: dest_off"
-                assert np.array_equal(sp[sl], rk["send_pair"]), f"iter {t} rank {v}: send_pair"
-                assert np.array_equal(_u32(sg[sl]), _u32(rk["send_gate"])), f"iter {t}: send_gate"
+                nk = len(rk["send_pair"])  # kept pairs (all of them without capacity)
+                assert np.array_equal(sp[sl][:nk], rk["send_pair"]), f"iter {t} rank {v}: send_pair"
+                assert np.array_equal(_u32(sg[sl][:nk]), _u32(rk["send_gate"])), f"iter {t}: send_gate"
                 GS = G * S
                 assert np.array_equal(sc[v * GS:(v + 1) * GS], rk["send_count"]), f"iter {t}: send_count"
         # optimizer state, bitwise (north_star: within 1e-6; the O6 op order makes it bitwise)

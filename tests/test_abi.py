@@ -37,7 +37,7 @@ def test_exports_every_declared_symbol(lib):
     assert declared == set(_lib.EXPORTED)
     for name in declared:
         assert hasattr(lib, name), name
-    assert lib.moe_abi_version() == 2
+    assert lib.moe_abi_version() == 3
     assert lib.moe_status_str(3) == b"MOE_ERR_DATA"
     assert lib.moe_ctx_handle_bytes() >= 3 * 64
 
@@ -97,6 +97,24 @@ def test_moe_plan_errors(lib):
     st = lib.moe_plan_ex(np.ones(2, np.int64).ctypes.data_as(C.POINTER(C.c_int64)), 2, 1, 4, 7,
                          C.byref(plan.c), None)
     assert st == 1
+
+
+def test_static_policy_and_capacity_through_abi(lib):
+    """Row f2 host logic: MOE_PLAN_STATIC equals the oracle's static policy; moe_slot_capacity
+    equals the oracle's formula (SPEC.md:201-203 examples included)."""
+    from paper_2504_19925_b200 import api
+    from oracle.dispatch import slot_capacity
+    for E, G, S in [(4, 2, 4), (5, 1, 8), (16, 8, 8), (128, 8, 32)]:
+        p = api.moe_plan(np.zeros(E, np.int64), E, G, S, policy=api.MOE_PLAN_STATIC)
+        assert p.replicas.tolist() == OP.static(E, G, S).tolist()
+    assert api.moe_slot_capacity(1.0, 4096, 1, 8, 8) == 64
+    assert api.moe_slot_capacity(1.0, 100, 1, 8, 8) == 1
+    assert api.moe_slot_capacity(2.0, 4096, 1, 8, 8) == 128
+    rng = np.random.default_rng(0)
+    for _ in range(500):
+        cf = float(rng.uniform(0.1, 4.0))
+        T, k, G, S = int(rng.integers(0, 10**6)), int(rng.integers(1, 9)), int(rng.integers(1, 9)), int(rng.integers(1, 64))
+        assert api.moe_slot_capacity(cf, T, k, G, S) == slot_capacity(cf, T, k, G * S)
 
 
 def test_spec_examples_through_abi(lib, golden_dir):

@@ -91,6 +91,29 @@ def test_dedup_is_bit_identical(name, G, iters, sampled):
     run_parity(name, G, iters, dedup=True, idx=_sample_idx(wl.P, G) if sampled else None)
 
 
+@pytest.mark.parametrize("name,G,cf", [("tiny-skew", 4, 1.0), ("tiny-odd", 3, 0.5), ("medium", 4, 1.25),
+                                       ("medium", 1, 1.0)])
+def test_capacity_and_drops(name, G, cf):
+    """Row f2: per-replica capacity; dropped pairs, kept send order, kept loads and per-expert
+    drops equal the oracle's, every iteration."""
+    from gpu_helpers import run_parity
+    from paper_2504_19925_b200 import moe_slot_capacity
+    from oracle.dispatch import slot_capacity
+    wl = configs.CONFIGS[name]
+    cap = moe_slot_capacity(cf, wl.T, wl.k, G, wl.S(G))
+    assert cap == slot_capacity(cf, wl.T, wl.k, wl.slots_total)
+    run_parity(name, G, 6, capacity=cap)
+
+
+@pytest.mark.parametrize("policy,interval", [(2, 1), (0, 3), (1, 2)])
+def test_static_and_interval_policies(policy, interval):
+    """Row f2: the static baseline (uniform replication) and interval re-placement."""
+    from gpu_helpers import run_parity
+    wl = configs.CONFIGS["tiny-skew"]
+    cap = 1 + wl.T * wl.k // wl.slots_total
+    run_parity("tiny-skew", 4, 7, policy=policy, replan_interval=interval, capacity=cap)
+
+
 def test_split_calls_equal_native_step_and_timing_hooks():
     """moe_step (native a0..a5) == moe_dispatch + moe_ctx_wait_counts + moe_plan + moe_update,
     bitwise; the timing hooks count one dispatch and one update launch per iteration."""
