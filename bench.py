@@ -240,8 +240,12 @@ def gpu_arm(args, wl):
     S = wl.S(G)
     Tg = wl.tokens_per_rank(G)
     seed = configs.seed_for(wl.name)
+    pol = {"alg1": api.MOE_PLAN_PAPER_ALG1, "minmax": api.MOE_PLAN_MINMAX,
+           "static": api.MOE_PLAN_STATIC}[args.policy]
+    cap = api.moe_slot_capacity(args.cf, wl.T, wl.k, G, S) if args.cf > 0 else 0
     layer = DecoupledExpertLayer(wl.E, G, S, wl.k, wl.P, Tg, rank=rank if G > 1 else 0,
-                                 device=local, seed=seed, dedup=args.dedup)
+                                 device=local, seed=seed, dedup=args.dedup, policy=pol,
+                                 capacity=cap, replan_interval=args.interval)
     if G > 1:
         layer.connect()
     n_tr = min(args.warmup + args.steps, args.trace_iters)
@@ -379,7 +383,8 @@ def gpu_arm(args, wl):
             "steps": K, "warmup": args.warmup, "ms_per_step": round(ms_iter, 4),
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (walk-spike routing trace, counter-hash grads)",
-            "config": dict(_config(wl, G), dedup=bool(args.dedup)),
+            "config": dict(_config(wl, G), dedup=bool(args.dedup), policy=args.policy,
+                           replan_interval=args.interval, capacity_factor=args.cf or None),
             "roofline": roof,
             "step_roofline": {"t_roof_ms": round(t_roof_step * 1e3, 4),
                               "frac": round(t_roof_step * 1e3 / ms_iter, 4),
@@ -414,6 +419,10 @@ def main():
     ap.add_argument("--dedup", default="auto", choices=["auto", "on", "off"],
                     help="locality de-duplication (MOE_OPT_DEDUP, SURVEY row f1): auto = on when "
                          "G > 1 (it moves fewer NVLink bytes; bit-identical results)")
+    ap.add_argument("--policy", default="alg1", choices=["alg1", "minmax", "static"],
+                    help="placement policy (row f2: static = uniform baseline)")
+    ap.add_argument("--interval", type=int, default=1, help="re-place every i iterations (row f2)")
+    ap.add_argument("--cf", type=float, default=0.0, help="capacity factor; 0 = drop-free (row f2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-iters", type=int, default=3)
     ap.add_argument("--cpu-frac", type=int, default=64)

@@ -126,3 +126,37 @@ def dispatch(ids_per_rank, gates_per_rank, first_slot, E: int, capacity: int = 0
         })
         base += n
     return out
+
+
+def drops_from_counts(C, replicas, capacity: int) -> np.ndarray:
+    """Per-expert drops of one iteration from the counts alone (row f2, reading B1): expert e's
+    r_e replicas hold q+1 (the first m) or q pairs (A8), and each keeps at most `capacity`,
+    so drops_e = m * max(0, q+1-cap) + (r_e-m) * max(0, q-cap).  Equals dispatch()'s drops."""
+    C = np.asarray(C, dtype=np.int64)
+    r = np.asarray(replicas, dtype=np.int64)
+    q, m = C // r, C % r
+    if capacity <= 0:
+        return np.zeros_like(C)
+    return m * np.maximum(0, q + 1 - capacity) + (r - m) * np.maximum(0, q - capacity)
+
+
+def policy_drops(counts_seq, E: int, G: int, S: int, capacity: int, policy: str = "alg1",
+                 interval: int = 1) -> dict:
+    """Drops of a whole trace under a placement policy (row f2; SPEC.md:485-548 policies):
+    plan_0 = uniform (reading A3); after iteration t the placement is recomputed from C_t when
+    (t+1) % interval == 0 (interval 1 = the paper's per-iteration policy), else kept.
+    Returns per-iteration drops, pairs, and the churn (slots changing expert) at each re-plan."""
+    from . import plan as _plan
+    p = _plan.plan(np.ones(E, dtype=np.int64), E, G, S, policy)
+    drops, pairs, churn = [], [], []
+    for t, C in enumerate(counts_seq):
+        C = np.asarray(C, dtype=np.int64)
+        drops.append(int(drops_from_counts(C, p["replicas"], capacity).sum()))
+        pairs.append(int(C.sum()))
+        if (t + 1) % interval == 0:
+            nxt = _plan.plan(C, E, G, S, policy)
+            churn.append(_plan.churn(p["slot_expert"], nxt["slot_expert"]))
+            p = nxt
+        else:
+            churn.append(0)
+    return {"drops": np.array(drops), "pairs": np.array(pairs), "churn": np.array(churn)}

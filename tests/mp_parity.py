@@ -28,6 +28,9 @@ def main() -> int:
     ap.add_argument("--sampled", action="store_true", help="compare a sample of elements only")
     ap.add_argument("--trace", default="config", choices=["config", "rotating-hot"])
     ap.add_argument("--dedup", action="store_true", help="MOE_OPT_DEDUP (row f1)")
+    ap.add_argument("--cf", type=float, default=0.0, help="capacity factor (row f2); 0 = none")
+    ap.add_argument("--policy", type=int, default=0, help="0 alg1, 1 minmax, 2 static")
+    ap.add_argument("--interval", type=int, default=1, help="re-placement interval (row f2)")
     args = ap.parse_args()
     rank, G, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -46,8 +49,11 @@ def main() -> int:
     Tg = wl.tokens_per_rank(G)
     Pg = P // G
     seed = configs.seed_for(wl.name)
+    from oracle.dispatch import slot_capacity
+    cap = slot_capacity(args.cf, wl.T, k, G * S) if args.cf > 0 else 0
     layer = DecoupledExpertLayer(E, G, S, k, P, Tg, rank=rank, device=local, seed=seed,
-                                 dedup=args.dedup)
+                                 dedup=args.dedup, capacity=cap, policy=args.policy,
+                                 replan_interval=args.interval)
     layer.connect()
     if args.sampled:
         rng = np.random.default_rng(1)
@@ -55,7 +61,9 @@ def main() -> int:
                                         np.arange(G) * Pg, np.arange(1, G + 1) * Pg - 1]))
     else:
         idx = np.arange(P)
-    sim = ostep.OracleSim(E, G, S, P, seed, idx=idx)
+    sim = ostep.OracleSim(E, G, S, P, seed, idx=idx, capacity=cap,
+                          policy={0: "alg1", 1: "minmax", 2: "static"}[args.policy],
+                          replan_interval=args.interval)
     idx_t = torch.from_numpy(idx).cuda()
     if args.trace == "rotating-hot":
         tr = traces.rotating_hot(E, wl.T, k, args.iters, seed=seed, hot_weight=4 if E < 16 else 16)
@@ -88,10 +96,15 @@ def main() -> int:
         rk = d["ranks"][rank]
         expect(layer.out.counts_host.tolist() == d["C"].tolist(), f"iter {t}: counts")
         expect(layer.out.slot_load.cpu().tolist() == d["slot_load"].tolist(), f"iter {t}: slot_load")
-        for name in ("dest_slot", "dest_off", "send_pair", "send_count"):
+        if cap > 0:
+            expect(layer.out.drops.cpu().tolist() == d["drops"].tolist(), f"iter {t}: drops")
+        nk = len(rk["send_pair"])          # kept pairs; the tail past them is unspecified
+        for name in ("dest_slot", "dest_off", "send_count"):
             got = getattr(layer.out, name).cpu().numpy()
             expect(np.array_equal(got, rk[name]), f"iter {t}: {name}")
-        expect(np.array_equal(layer.out.send_gate.cpu().numpy().view(np.uint32),
+        expect(np.array_equal(layer.out.send_pair.cpu().numpy()[:nk], rk["send_pair"]),
+               f"iter {t}: send_pair")
+        expect(np.array_equal(layer.out.send_gate.cpu().numpy()[:nk].view(np.uint32),
                               rk["send_gate"].view(np.uint32)), f"iter {t}: send_gate")
         sel = (idx >= rank * Pg) & (idx < (rank + 1) * Pg)
         li = torch.from_numpy(idx[sel] - rank * Pg).cuda()

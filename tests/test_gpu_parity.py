@@ -224,3 +224,12 @@ def test_full_size_sampled(name, G, iters):
     from gpu_helpers import run_parity
     wl = configs.CONFIGS[name]
     run_parity(name, G, iters, idx=_sample_idx(wl.P, G))
+
+
+@pytest.mark.parametrize("policy,interval", [("alg1", 1), ("alg1", 10), ("static", 1)])
+def test_policy_drops_long_horizon(policy, interval):
+    """Row f2 over 150 iterations of the paper's setup (E = 16, 64 slots, cf = 1.0): the CUDA
+    dispatch's drops and the re-placement churn equal the oracle's every iteration."""
+    from policy_study import run
+    r = run(1, 150, policy, interval)
+    assert r["pairs"] == 150 * 4096 * 2

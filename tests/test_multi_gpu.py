@@ -32,6 +32,9 @@ def _torchrun(n: int, *args, timeout=600):
     (2, "medium", ["--dedup", "--iters", "4"]), (4, "medium", ["--dedup", "--iters", "4"]),
     (4, "tiny-skew", ["--dedup", "--trace", "rotating-hot"]),
     (4, "gpt-small", ["--dedup", "--sampled", "--iters", "3"]),
+    (2, "tiny", ["--cf", "0.5"]), (4, "medium", ["--cf", "1.25", "--dedup", "--iters", "4"]),
+    (4, "tiny-skew", ["--cf", "1.0", "--policy", "2"]),
+    (4, "tiny-skew", ["--cf", "1.0", "--interval", "3", "--iters", "7", "--dedup"]),
 ])
 def test_real_multi_gpu_parity(G, config, extra):
     if torch.cuda.device_count() < G:

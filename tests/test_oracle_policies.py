@@ -1,0 +1,76 @@
+"""Row f2 at the count level: per-expert drops under a capacity, and the policy ordering the
+paper's evaluation reports (PAPER.md:1081-1087, 1126-1132 fig:eval_survived; SPEC.md:755
+acceptance 6 as a property, since the paper's absolute percentages need real training)."""
+import numpy as np
+import pytest
+
+from oracle import dispatch as OD
+from oracle import plan as OP
+from synth import traces
+
+
+def test_drops_from_counts_equals_full_dispatch():
+    """The closed form (q/q+1 loads, keep < cap) against the pair-by-pair dispatch."""
+    rng = np.random.default_rng(7)
+    for it in range(60):
+        E = int(rng.integers(1, 9))
+        G = int(rng.integers(1, 4))
+        S = int(rng.integers(-(-E // G), -(-E // G) + 4))
+        T, k = int(rng.integers(0, 300)) * G, int(rng.integers(1, E + 1))
+        ids = np.stack([rng.permutation(E)[:k] for _ in range(T)]).astype(np.int32).reshape(T, k)
+        gates = rng.random((T, k)).astype(np.float32)
+        c = rng.integers(0, 50, E)
+        p = OP.plan(c, E, G, S, "alg1" if it % 2 else "minmax")
+        cap = int(rng.integers(1, 2 + T * k // (G * S) if T else 3))
+        d = OD.dispatch(traces.split_ranks(ids, G), traces.split_ranks(gates, G), p["first_slot"], E, cap)
+        assert OD.drops_from_counts(d["C"], p["replicas"], cap).tolist() == d["drops"].tolist()
+        # brute force: a pair is dropped iff its offset in its replica is >= cap
+        dropped = sum(int((rk["dest_slot"] < 0).sum()) for rk in d["ranks"])
+        assert dropped == int(d["drops"].sum())
+        assert int(d["slot_load"].sum()) + dropped == T * k
+        assert (d["slot_load"] <= cap).all()
+
+
+def test_drop_free_without_or_above_capacity():
+    C = np.array([100, 3, 0, 7])
+    r = np.array([3, 1, 1, 1])
+    assert OD.drops_from_counts(C, r, 0).tolist() == [0, 0, 0, 0]
+    assert OD.drops_from_counts(C, r, 34).tolist() == [0, 0, 0, 0]
+    # 100 over 3 replicas = 34, 33, 33; cap 33 drops 1; cap 1 drops 97
+    assert OD.drops_from_counts(C, r, 33).tolist() == [1, 0, 0, 0]
+    assert OD.drops_from_counts(C, r, 1).tolist() == [97, 2, 0, 6]
+
+
+def test_policy_mechanics_static_and_interval():
+    """static never changes; interval(i) re-plans only after iterations
+    t with (t+1) % i == 0; per-iteration plan_{t+1} = Alg1(C_t)."""
+    E, G, S = 8, 2, 8
+    tr = traces.walk_spike(E, 512, 2, 30, seed=11)
+    Cs = [traces.expert_counts(ids, E) for ids, _ in tr]
+    st = OD.policy_drops(Cs, E, G, S, 64, "static")
+    assert (st["churn"] == 0).all()
+    iv = OD.policy_drops(Cs, E, G, S, 64, "alg1", interval=7)
+    assert all(c == 0 for t, c in enumerate(iv["churn"]) if (t + 1) % 7)
+    per = OD.policy_drops(Cs, E, G, S, 64, "alg1")
+    for t in range(1, len(Cs)):
+        r = OP.alg1(Cs[t - 1], E, G, S)
+        assert per["drops"][t] == int(OD.drops_from_counts(Cs[t], r, 64).sum())
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_drop_ordering_per_iteration_interval_static(seed):
+    """SPEC acceptance 6 shape at the paper's setup (E = 16 classes, s = 4 slots on N = 16
+    ranks, cf = 1.0, 2,000 iterations) on a seeded spiky trace: aggregate drops
+    per-iteration < interval(10) <= interval(50) <= interval(100) < static, with 1 pp slack on
+    the <= and a >= 10 pp margin between per-iteration and static."""
+    E, G, S, T, k = 16, 16, 4, 1024, 2
+    cap = OD.slot_capacity(1.0, T, k, G * S)
+    Cs = [traces.expert_counts(ids, E) for ids, _ in traces.walk_spike(E, T, k, 2000, seed=seed)]
+    rate = {}
+    for name, pol, iv in [("per", "alg1", 1), ("i10", "alg1", 10), ("i50", "alg1", 50),
+                          ("i100", "alg1", 100), ("static", "static", 1)]:
+        r = OD.policy_drops(Cs, E, G, S, cap, pol, iv)
+        rate[name] = 100.0 * r["drops"].sum() / r["pairs"].sum()
+    assert rate["per"] < rate["i10"] <= rate["i50"] + 1 and rate["i50"] <= rate["i100"] + 1
+    assert rate["i100"] < rate["static"]
+    assert rate["static"] - rate["per"] >= 10, rate
