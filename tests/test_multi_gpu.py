@@ -35,7 +35,7 @@ def _torchrun(n: int, *args, timeout=600):
     (2, "tiny", ["--cf", "0.5"]), (4, "medium", ["--cf", "1.25", "--dedup", "--iters", "4"]),
     (4, "tiny-skew", ["--cf", "1.0", "--policy", "2"]),
     (4, "tiny-skew", ["--cf", "1.0", "--interval", "3", "--iters", "7", "--dedup"]),
-])
+], ids=lambda x: "".join(a.lstrip("-") for a in x) if isinstance(x, list) else str(x))
 def test_real_multi_gpu_parity(G, config, extra):
     if torch.cuda.device_count() < G:
         pytest.skip(f"needs {G} GPUs")
