@@ -9,5 +9,6 @@ library raises.
 from .api import (AdamConfig, DispatchBuffers, MoeContext, MoeError, Plan,  # noqa: F401
                   MOE_OPT_DEDUP, MOE_PLAN_KEEP, MOE_PLAN_MINMAX, MOE_PLAN_PAPER_ALG1,
                   MOE_PLAN_STATIC, moe_dispatch, moe_place, moe_plan, moe_slot_capacity, moe_step,
-                  moe_update, synth_grads, synth_master)
+                  moe_update, synth_grads, synth_master, TokenExchange, MOE_TOK_GATE,
+                  moe_token_dispatch, moe_token_combine)
 from .layer import DecoupledExpertLayer  # noqa: F401

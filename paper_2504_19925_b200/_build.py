@@ -22,10 +22,10 @@ INC = os.path.join(ROOT, "include")
 OUT = os.path.join(HERE, "libmoedc.so")
 OBJ = os.path.join(HERE, "build")
 
-CU = ["ctx.cu", "dispatch.cu", "update.cu", "synth.cu"]
+CU = ["ctx.cu", "dispatch.cu", "update.cu", "synth.cu", "tokens.cu"]
 CPP = ["plan.cpp", "step.cpp"]
 HEADERS = [os.path.join(CSRC, h) for h in ("common.h", "internal.h")] + \
-    [os.path.join(INC, h) for h in ("moe_dc.h", "moe_synth.h")]
+    [os.path.join(INC, h) for h in ("moe_dc.h", "moe_synth.h", "moe_tokens.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -1,4 +1,4 @@
-"""ctypes view of include/moe_dc.h and include/moe_synth.h (argument marshalling only).
+"""ctypes view of include/moe_dc.h, moe_synth.h and moe_tokens.h (argument marshalling only).
 
 Loads the in-tree ``libmoedc.so``.  There is no fallback: if the library is missing the
 import fails loudly (build it with ``__graft_entry__.build()``).
@@ -25,7 +25,10 @@ EXPORTED = [
     "moe_ctx_connect", "moe_ctx_check", "moe_ctx_wait_counts", "moe_dispatch", "moe_update",
     "moe_place", "moe_step", "moe_ctx_set_timing", "moe_ctx_get_timing", "moe_ctx_get_timing_ex",
     "moe_synth_grads", "moe_synth_master",
+    "moe_tokx_create", "moe_tokx_destroy", "moe_tokx_handle_bytes", "moe_tokx_export",
+    "moe_tokx_connect", "moe_token_dispatch", "moe_token_combine",
 ]
+MOE_TOK_GATE = 1
 
 _i32p = C.POINTER(C.c_int32)
 _i64p = C.POINTER(C.c_int64)
@@ -123,6 +126,21 @@ def lib() -> C.CDLL:
         L.moe_synth_master.restype = C.c_int
         L.moe_synth_master.argtypes = [C.c_void_p, C.c_uint64, C.c_int32, C.c_int64, C.c_int64,
                                        C.c_void_p]
+        L.moe_tokx_create.restype = C.c_int
+        L.moe_tokx_create.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.POINTER(C.c_void_p),
+                                      C.POINTER(C.c_void_p)]
+        L.moe_tokx_destroy.restype = C.c_int
+        L.moe_tokx_destroy.argtypes = [C.c_void_p]
+        L.moe_tokx_handle_bytes.restype = C.c_int
+        L.moe_tokx_handle_bytes.argtypes = []
+        L.moe_tokx_export.restype = C.c_int
+        L.moe_tokx_export.argtypes = [C.c_void_p, C.c_void_p]
+        L.moe_tokx_connect.restype = C.c_int
+        L.moe_tokx_connect.argtypes = [C.c_void_p, C.c_void_p]
+        for f in (L.moe_token_dispatch, L.moe_token_combine):
+            f.restype = C.c_int
+            f.argtypes = [C.c_void_p, C.POINTER(C.c_void_p), C.c_int64, C.c_void_p,
+                          C.POINTER(MoeDispatchOut), C.c_int32, C.c_void_p]
         _lib = L
     return _lib
 

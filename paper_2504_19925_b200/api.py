@@ -282,3 +282,89 @@ def synth_grads(dst: torch.Tensor, seed: int, t: int, slot_base: int, S: int, P:
 def synth_master(dst: torch.Tensor, seed: int, E: int, lo: int, n: int, stream=None) -> None:
     check(L.lib().moe_synth_master(_ptr(dst), seed, E, lo, n, _stream_ptr(stream)),
           "moe_synth_master")
+
+
+# ---- row f3: token all-to-all (include/moe_tokens.h) -----------------------------------------
+MOE_TOK_GATE = L.MOE_TOK_GATE
+
+
+class TokenExchange:
+    """moe_tokx: expert buffers xbuf [S][rows][d] bf16 (one per local rank) bound to a context.
+
+    Real mode with G > 1: call connect_process_group() on every rank before the first use."""
+
+    def __init__(self, ctx: MoeContext, d: int, rows: int, xbuf=None):
+        dev = torch.device("cuda", ctx.device)
+        if xbuf is None:
+            xbuf = [torch.zeros(ctx.S * rows * d, dtype=torch.bfloat16, device=dev)
+                    for _ in range(ctx.n_local)]
+        if len(xbuf) != ctx.n_local:
+            raise ValueError(f"xbuf: expected {ctx.n_local} tensors")
+        for t in xbuf:
+            if t.dtype != torch.bfloat16 or t.numel() != ctx.S * rows * d or not t.is_contiguous():
+                raise ValueError("xbuf: contiguous bf16 [S][rows][d]")
+        self.ctx, self.d, self.rows, self.xbuf = ctx, d, rows, list(xbuf)
+        self._arr = (C.c_void_p * ctx.n_local)(*[t.data_ptr() for t in self.xbuf])
+        h = C.c_void_p()
+        check(L.lib().moe_tokx_create(ctx.handle, d, rows, self._arr, C.byref(h)), "moe_tokx_create")
+        self._h = h
+
+    @property
+    def handle(self) -> C.c_void_p:
+        if self._h is None:
+            raise RuntimeError("token exchange destroyed")
+        return self._h
+
+    def export(self) -> bytes:
+        buf = C.create_string_buffer(L.lib().moe_tokx_handle_bytes())
+        check(L.lib().moe_tokx_export(self.handle, buf), "moe_tokx_export")
+        return buf.raw
+
+    def connect(self, records: list[bytes]) -> None:
+        blob = b"".join(records)
+        check(L.lib().moe_tokx_connect(self.handle, C.create_string_buffer(blob, len(blob))),
+              "moe_tokx_connect")
+
+    def connect_process_group(self, group=None) -> None:
+        if self.ctx.rank >= 0 and self.ctx.G > 1:
+            self.connect(gather_records(self.export(), self.ctx.G, group))
+
+    def slot_view(self, v: int = 0) -> torch.Tensor:
+        """Local rank v's expert buffer as [S][rows][d]."""
+        return self.xbuf[v].view(self.ctx.S, self.rows, self.d)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None:
+            L.lib().moe_tokx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _tok_ptrs(x: TokenExchange, tensors, T: int, what: str):
+    if len(tensors) != x.ctx.n_local:
+        raise ValueError(f"{what}: expected {x.ctx.n_local} tensors")
+    for t in tensors:
+        if t.dtype != torch.bfloat16 or t.numel() != T * x.d or not t.is_contiguous():
+            raise ValueError(f"{what}: contiguous bf16 [T][d]")
+    return (C.c_void_p * len(tensors))(*[t.data_ptr() for t in tensors])
+
+
+def moe_token_dispatch(x: TokenExchange, src, T: int, out: DispatchBuffers, gates=None,
+                       flags: int = 0, stream=None) -> None:
+    """Token rows -> xbuf[dest_slot][dest_off] (reading C1); MOE_TOK_GATE scales by the gate."""
+    arr = _tok_ptrs(x, src, T, "src")
+    check(L.lib().moe_token_dispatch(x.handle, arr, T, _ptr(gates), C.byref(out.c), flags,
+                                     _stream_ptr(stream)), "moe_token_dispatch")
+
+
+def moe_token_combine(x: TokenExchange, dst, T: int, out: DispatchBuffers, gates=None,
+                      flags: int = 0, stream=None) -> None:
+    """dst[t] = bf16(sum_j [gate_j *] xbuf[dest_slot][dest_off]) (reading C2)."""
+    arr = _tok_ptrs(x, dst, T, "dst")
+    check(L.lib().moe_token_combine(x.handle, arr, T, _ptr(gates), C.byref(out.c), flags,
+                                    _stream_ptr(stream)), "moe_token_combine")

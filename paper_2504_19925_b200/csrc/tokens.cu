@@ -1,0 +1,438 @@
+// Row f3: token all-to-all along the replica-balanced dispatch (include/moe_tokens.h).
+//
+// PAPER.md:145 (tokens to the experts' devices and back, 2 fwd + 2 bwd all-to-alls),
+// PAPER.md:169 + 690-692 (balanced over replicas by the a2 dispatch).  Readings C1-C3
+// (DESIGN.md): dispatch copies token rows into xbuf[dest_slot][dest_off] (optionally
+// gate-scaled, bf16 RNE); combine sums the k rows of a token in ascending j, fp32 from +0.0,
+// optionally gate-weighted, and rounds to bf16 RNE.
+//
+// B200 design: both are HBM/NVLink-bound copies, so no tensor cores and no staging beyond
+// registers.  One warp per token:
+//   dispatch -- reads the token row ONCE (16-byte loads, 4 vectors per lane in flight) and
+//               stores it to each of its k destinations: local HBM or a peer's HBM through the
+//               NVLink mapping (plain 16-byte stores; a warp writes 512 contiguous bytes).
+//               Reading each row once instead of once per pair halves the local read traffic.
+//   combine  -- pulls the k rows (peer loads) and accumulates in registers; one bf16 store.
+// Grids are persistent (blocks_per_sm x SMs, grid-stride over tokens).
+// Cross-GPU ordering (real mode, G > 1) uses system-scope flags in a small per-GPU sync
+// buffer mapped by every peer (CUDA IPC), like the update kernel's barriers:
+//   arrive -- every call: CTA 0 of each rank releases arrive[rank] = epoch on every GPU, and
+//             every CTA acquires all G arrive flags before touching a peer's buffer.  Stream
+//             order makes "arrived" mean "all my earlier kernels (the FFN writes, the previous
+//             combine's reads) are complete".
+//   done   -- dispatch only: each CTA fences its stores at system scope and takes a ticket;
+//             the last CTA releases done[rank] on every GPU; a 1-CTA kernel then waits for
+//             all G, so work enqueued after moe_token_dispatch sees every rank's rows.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <string>
+
+#include "internal.h"
+#include "moe_tokens.h"
+
+using namespace moe;
+
+namespace {
+
+struct TokSync {
+  alignas(128) uint32_t arrive[MOE_MAX_G];
+  alignas(128) uint32_t done[MOE_MAX_G];
+  alignas(128) uint32_t ticket;
+};
+
+struct TokIpc {
+  cudaIpcMemHandle_t h[2];  // xbuf, sync
+  uint64_t off[2];
+  int64_t d, rows;
+};
+
+constexpr int kTokU = 4;  // 16-byte vectors per lane in flight
+
+}  // namespace
+
+struct moe_tokx {
+  moe_ctx *ctx;
+  int64_t d, rows, dv;  // dv = d / 8 vectors per row
+  std::vector<void *> xbuf;                  // [n_local] caller buffers
+  void *peer_xbuf[MOE_MAX_G];
+  TokSync *peer_sync[MOE_MAX_G];
+  TokSync *sync;                             // this GPU's (virtual: the single one)
+  uint32_t arrive_epoch, done_epoch;
+  int blocks;
+  bool connected;
+  std::map<std::string, void *> opened;
+};
+
+namespace {
+
+struct TokArgs {
+  const uint4 *src[MOE_MAX_G];   // dispatch: [n_local] bf16 [T][d]
+  uint4 *dst[MOE_MAX_G];         // combine:  [n_local] bf16 [T][d]
+  uint4 *xb[MOE_MAX_G];          // per GPU h: its expert buffer [S][rows][d]
+  TokSync *psync[MOE_MAX_G];     // per GPU h
+  const int32_t *dest_slot, *dest_off;  // [n_local][T*k]
+  const float *gates;                   // [n_local][T*k] (MOE_TOK_GATE)
+  int64_t T, rows, dv;
+  int k, S, n_local, gate;
+  int G, rank;                   // rank < 0: virtual (no flags)
+  uint32_t epoch;
+  int32_t *err;
+};
+
+__device__ __forceinline__ void arrive_and_wait(const TokArgs &a) {
+  if (a.rank < 0 || a.G == 1) return;
+  if (blockIdx.x == 0 && threadIdx.x < a.G) st_release_sys(&a.psync[threadIdx.x]->arrive[a.rank], a.epoch);
+  if (threadIdx.x < a.G) wait_flag(&a.psync[a.rank]->arrive[threadIdx.x], a.epoch, a.err);
+  __syncthreads();
+}
+
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+
+// fp32 -> bf16 RNE, NaN -> 0x7FFF (reading A17)
+__device__ __forceinline__ uint32_t rne16(float f) {
+  const uint32_t u = __float_as_uint(f);
+  if ((u & 0x7FFFFFFFu) > 0x7F800000u) return 0x7FFFu;
+  return (u + 0x7FFFu + ((u >> 16) & 1u)) >> 16;
+}
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) { return rne16(lo) | (rne16(hi) << 16); }
+
+__device__ __forceinline__ uint4 scale8(uint4 v, float g) {
+  uint4 r;
+  r.x = pack2(__fmul_rn(bf_lo(v.x), g), __fmul_rn(bf_hi(v.x), g));
+  r.y = pack2(__fmul_rn(bf_lo(v.y), g), __fmul_rn(bf_hi(v.y), g));
+  r.z = pack2(__fmul_rn(bf_lo(v.z), g), __fmul_rn(bf_hi(v.z), g));
+  r.w = pack2(__fmul_rn(bf_lo(v.w), g), __fmul_rn(bf_hi(v.w), g));
+  return r;
+}
+
+__device__ __forceinline__ uint4 ldg_nc(const uint4 *p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+
+__global__ void __launch_bounds__(kThreads) k_tok_dispatch(TokArgs a) {
+  arrive_and_wait(a);
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (kThreads / 32);
+  const int64_t ntok = a.T * a.n_local;
+  for (int64_t w = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); w < ntok; w += warps) {
+    const int v = (int)(w / a.T);
+    const int64_t t = w - (int64_t)v * a.T;
+    const int64_t pbase = (int64_t)v * a.T * a.k + t * a.k;
+    const uint4 *src = a.src[v] + t * a.dv;
+    for (int64_t c0 = 0; c0 < a.dv; c0 += 32 * kTokU) {
+      uint4 x[kTokU];
+#pragma unroll
+      for (int u = 0; u < kTokU; ++u) {
+        const int64_t c = c0 + u * 32 + lane;
+        if (c < a.dv) x[u] = ldg_nc(src + c);
+      }
+      for (int j = 0; j < a.k; ++j) {
+        const int s = __ldg(a.dest_slot + pbase + j);
+        if (s < 0) continue;  // dropped (reading B1)
+        const int off = __ldg(a.dest_off + pbase + j);
+        if (off >= a.rows) {
+          if (lane == 0 && c0 == 0) atomicOr(a.err, kErrData);
+          continue;
+        }
+        uint4 *dst = a.xb[s / a.S] + ((int64_t)(s % a.S) * a.rows + off) * a.dv;
+        const float g = a.gate ? __ldg(a.gates + pbase + j) : 1.f;
+#pragma unroll
+        for (int u = 0; u < kTokU; ++u) {
+          const int64_t c = c0 + u * 32 + lane;
+          if (c < a.dv) dst[c] = a.gate ? scale8(x[u], g) : x[u];
+        }
+      }
+    }
+  }
+  if (a.rank >= 0 && a.G > 1) {  // barrier-out: the last CTA announces "my rows landed"
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const uint32_t tk = atomicAdd(&a.psync[a.rank]->ticket, 1u);
+      if (tk == gridDim.x - 1) {
+        a.psync[a.rank]->ticket = 0;
+        __threadfence_system();
+        for (int h = 0; h < a.G; ++h) st_release_sys(&a.psync[h]->done[a.rank], a.epoch);
+      }
+    }
+  }
+}
+
+__global__ void k_tok_wait_done(TokSync *mine, int G, uint32_t epoch, int32_t *err) {
+  if ((int)threadIdx.x < G) wait_flag(&mine->done[threadIdx.x], epoch, err);
+}
+
+__global__ void __launch_bounds__(kThreads) k_tok_combine(TokArgs a) {
+  arrive_and_wait(a);
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (kThreads / 32);
+  const int64_t ntok = a.T * a.n_local;
+  for (int64_t w = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); w < ntok; w += warps) {
+    const int v = (int)(w / a.T);
+    const int64_t t = w - (int64_t)v * a.T;
+    const int64_t pbase = (int64_t)v * a.T * a.k + t * a.k;
+    uint4 *dst = a.dst[v] + t * a.dv;
+    for (int64_t c0 = 0; c0 < a.dv; c0 += 32 * kTokU) {
+      float acc[kTokU][8];
+#pragma unroll
+      for (int u = 0; u < kTokU; ++u)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[u][i] = 0.f;
+      for (int j = 0; j < a.k; ++j) {  // ascending j (reading C2)
+        const int s = __ldg(a.dest_slot + pbase + j);
+        if (s < 0) continue;
+        const int off = __ldg(a.dest_off + pbase + j);
+        if (off >= a.rows) {
+          if (lane == 0 && c0 == 0) atomicOr(a.err, kErrData);
+          continue;
+        }
+        const uint4 *row = a.xb[s / a.S] + ((int64_t)(s % a.S) * a.rows + off) * a.dv;
+        const float g = a.gate ? __ldg(a.gates + pbase + j) : 1.f;
+        uint4 y[kTokU];
+#pragma unroll
+        for (int u = 0; u < kTokU; ++u) {
+          const int64_t c = c0 + u * 32 + lane;
+          if (c < a.dv) y[u] = ldg_nc(row + c);  // rows are final before the arrive flags
+        }
+#pragma unroll
+        for (int u = 0; u < kTokU; ++u) {
+          const uint32_t wd[4] = {y[u].x, y[u].y, y[u].z, y[u].w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            float lo = bf_lo(wd[q]), hi = bf_hi(wd[q]);
+            if (a.gate) {
+              lo = __fmul_rn(g, lo);
+              hi = __fmul_rn(g, hi);
+            }
+            acc[u][2 * q] = __fadd_rn(acc[u][2 * q], lo);
+            acc[u][2 * q + 1] = __fadd_rn(acc[u][2 * q + 1], hi);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kTokU; ++u) {
+        const int64_t c = c0 + u * 32 + lane;
+        if (c < a.dv) {
+          uint4 o;
+          o.x = pack2(acc[u][0], acc[u][1]);
+          o.y = pack2(acc[u][2], acc[u][3]);
+          o.z = pack2(acc[u][4], acc[u][5]);
+          o.w = pack2(acc[u][6], acc[u][7]);
+          dst[c] = o;
+        }
+      }
+    }
+  }
+}
+
+typedef int (*PFN_getAddressRange)(unsigned long long *, size_t *, unsigned long long);
+
+int alloc_base(const void *ptr, void **base) {
+  static PFN_getAddressRange fn = nullptr;
+  if (!fn) {
+    void *f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    MOE_CUDA_TRY(cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q));
+    if (!f || q != cudaDriverEntryPointSuccess)
+      return fail(MOE_ERR_COMM, "cuMemGetAddressRange entry point unavailable");
+    fn = (PFN_getAddressRange)f;
+  }
+  unsigned long long b = 0;
+  size_t sz = 0;
+  if (fn(&b, &sz, (unsigned long long)ptr) != 0) return fail(MOE_ERR_COMM, "cuMemGetAddressRange failed");
+  *base = (void *)b;
+  return MOE_OK;
+}
+
+int fill_args(moe_tokx *x, int64_t T, const float *gates, const moe_dispatch_out *out, int32_t flags,
+              const char *what, TokArgs *a) {
+  moe_ctx *c = x->ctx;
+  if (!out || !out->dest_slot || !out->dest_off) return fail(MOE_ERR_INVALID, "%s: NULL dispatch outputs", what);
+  if (T < 0 || T > c->max_tokens) return fail(MOE_ERR_INVALID, "%s: T=%lld outside [0, max_tokens]", what, (long long)T);
+  if ((flags & MOE_TOK_GATE) && !gates) return fail(MOE_ERR_INVALID, "%s: MOE_TOK_GATE needs gates", what);
+  if (!x->connected) return fail(MOE_ERR_INVALID, "%s: call moe_tokx_connect first", what);
+  memset(a, 0, sizeof(*a));
+  for (int h = 0; h < c->G; ++h) {
+    a->xb[h] = (uint4 *)x->peer_xbuf[h];
+    a->psync[h] = x->peer_sync[h];
+  }
+  a->dest_slot = out->dest_slot;
+  a->dest_off = out->dest_off;
+  a->gates = gates;
+  a->T = T;
+  a->rows = x->rows;
+  a->dv = x->dv;
+  a->k = c->k;
+  a->S = c->S;
+  a->n_local = c->n_local;
+  a->gate = (flags & MOE_TOK_GATE) ? 1 : 0;
+  a->G = c->G;
+  a->rank = c->rank;
+  a->err = c->err;
+  return MOE_OK;
+}
+
+}  // namespace
+
+extern "C" int moe_tokx_create(moe_ctx *ctx, int64_t d, int64_t rows, void *const *xbuf, moe_tokx **out) {
+  if (!ctx || !xbuf || !out) return fail(MOE_ERR_INVALID, "moe_tokx_create: NULL argument");
+  *out = nullptr;
+  if (d < 8 || d % 8) return fail(MOE_ERR_INVALID, "moe_tokx_create: need d %% 8 == 0 and d >= 8");
+  if (rows < 1 || rows > ((int64_t)1 << 31)) return fail(MOE_ERR_INVALID, "moe_tokx_create: rows out of range");
+  for (int v = 0; v < ctx->n_local; ++v) {
+    if (!xbuf[v]) return fail(MOE_ERR_INVALID, "moe_tokx_create: NULL buffer for local rank %d", v);
+    if ((uintptr_t)xbuf[v] & 15) return fail(MOE_ERR_INVALID, "moe_tokx_create: buffers must be 16-byte aligned");
+  }
+  MOE_CUDA_TRY(cudaSetDevice(ctx->device));
+  moe_tokx *x = new moe_tokx();
+  x->ctx = ctx;
+  x->d = d;
+  x->rows = rows;
+  x->dv = d / 8;
+  x->arrive_epoch = x->done_epoch = 0;
+  for (int v = 0; v < ctx->n_local; ++v) x->xbuf.push_back(xbuf[v]);
+  for (int h = 0; h < MOE_MAX_G; ++h) {
+    x->peer_xbuf[h] = nullptr;
+    x->peer_sync[h] = nullptr;
+  }
+  x->sync = nullptr;
+  if (cudaMalloc(&x->sync, sizeof(TokSync)) != cudaSuccess || cudaMemset(x->sync, 0, sizeof(TokSync)) != cudaSuccess ||
+      cudaDeviceSynchronize() != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(x->sync);
+    delete x;
+    return fail(MOE_ERR_CUDA, "moe_tokx_create: cannot allocate the sync buffer");
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tok_combine, kThreads, 0);
+  x->blocks = ctx->num_sms * (per_sm > 0 ? per_sm : 1);
+  if (ctx->rank < 0) {
+    for (int h = 0; h < ctx->G; ++h) {
+      x->peer_xbuf[h] = x->xbuf[h];
+      x->peer_sync[h] = x->sync;
+    }
+    x->connected = true;
+  } else {
+    x->peer_xbuf[ctx->rank] = x->xbuf[0];
+    x->peer_sync[ctx->rank] = x->sync;
+    x->connected = (ctx->G == 1);
+  }
+  *out = x;
+  return MOE_OK;
+}
+
+extern "C" int moe_tokx_destroy(moe_tokx *x) {
+  if (!x) return MOE_OK;
+  cudaSetDevice(x->ctx->device);
+  for (auto &kv : x->opened) cudaIpcCloseMemHandle(kv.second);
+  cudaFree(x->sync);
+  delete x;
+  return MOE_OK;
+}
+
+extern "C" int moe_tokx_handle_bytes(void) { return (int)sizeof(TokIpc); }
+
+extern "C" int moe_tokx_export(moe_tokx *x, void *out) {
+  if (!x || !out) return fail(MOE_ERR_INVALID, "moe_tokx_export: NULL argument");
+  if (x->ctx->rank < 0) return fail(MOE_ERR_INVALID, "moe_tokx_export: virtual-mode context");
+  MOE_CUDA_TRY(cudaSetDevice(x->ctx->device));
+  TokIpc rec;
+  memset(&rec, 0, sizeof(rec));
+  const void *bufs[2] = {x->xbuf[0], x->sync};
+  for (int i = 0; i < 2; ++i) {
+    void *base = nullptr;
+    const int st = alloc_base(bufs[i], &base);
+    if (st) return st;
+    MOE_CUDA_TRY(cudaIpcGetMemHandle(&rec.h[i], base));
+    rec.off[i] = (uint64_t)((const char *)bufs[i] - (const char *)base);
+  }
+  rec.d = x->d;
+  rec.rows = x->rows;
+  memcpy(out, &rec, sizeof(rec));
+  return MOE_OK;
+}
+
+extern "C" int moe_tokx_connect(moe_tokx *x, const void *all) {
+  if (!x || !all) return fail(MOE_ERR_INVALID, "moe_tokx_connect: NULL argument");
+  moe_ctx *c = x->ctx;
+  if (c->rank < 0) return fail(MOE_ERR_INVALID, "moe_tokx_connect: virtual-mode context");
+  MOE_CUDA_TRY(cudaSetDevice(c->device));
+  const TokIpc *recs = (const TokIpc *)all;
+  for (int h = 0; h < c->G; ++h) {
+    if (recs[h].d != x->d || recs[h].rows != x->rows)
+      return fail(MOE_ERR_INVALID, "moe_tokx_connect: ranks disagree on (d, rows)");
+    if (h == c->rank) continue;
+    void *ptrs[2] = {nullptr, nullptr};
+    for (int i = 0; i < 2; ++i) {
+      std::string key((const char *)&recs[h].h[i], sizeof(cudaIpcMemHandle_t));
+      auto it = x->opened.find(key);
+      void *base = nullptr;
+      if (it != x->opened.end()) {
+        base = it->second;
+      } else {
+        const cudaError_t e = cudaIpcOpenMemHandle(&base, recs[h].h[i], cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess)
+          return fail(MOE_ERR_COMM, "cudaIpcOpenMemHandle(peer %d, token buffer %d): %s", h, i, cudaGetErrorString(e));
+        x->opened[key] = base;
+      }
+      ptrs[i] = (char *)base + recs[h].off[i];
+    }
+    x->peer_xbuf[h] = ptrs[0];
+    x->peer_sync[h] = (TokSync *)ptrs[1];
+  }
+  x->connected = true;
+  return MOE_OK;
+}
+
+extern "C" int moe_token_dispatch(moe_tokx *x, const void *const *src, int64_t T, const float *gates,
+                                  const moe_dispatch_out *out, int32_t flags, void *stream) {
+  if (!x || !src) return fail(MOE_ERR_INVALID, "moe_token_dispatch: NULL argument");
+  TokArgs a;
+  int st = fill_args(x, T, gates, out, flags, "moe_token_dispatch", &a);
+  if (st) return st;
+  moe_ctx *c = x->ctx;
+  for (int v = 0; v < c->n_local; ++v) {
+    if (!src[v] && T > 0) return fail(MOE_ERR_INVALID, "moe_token_dispatch: NULL src for local rank %d", v);
+    if ((uintptr_t)src[v] & 15) return fail(MOE_ERR_INVALID, "moe_token_dispatch: src must be 16-byte aligned");
+    a.src[v] = (const uint4 *)src[v];
+  }
+  MOE_CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool sync = c->rank >= 0 && c->G > 1;
+  a.epoch = sync ? ++x->arrive_epoch : 0;
+  k_tok_dispatch<<<x->blocks, kThreads, 0, s>>>(a);
+  MOE_CUDA_TRY(cudaGetLastError());
+  if (sync) {
+    // the done flags reuse the arrive epoch (one dispatch per arrive increment is enough:
+    // done[] is written only by dispatches, and epochs only grow)
+    k_tok_wait_done<<<1, 32, 0, s>>>(x->sync, c->G, a.epoch, c->err);
+    MOE_CUDA_TRY(cudaGetLastError());
+  }
+  return MOE_OK;
+}
+
+extern "C" int moe_token_combine(moe_tokx *x, void *const *dst, int64_t T, const float *gates,
+                                 const moe_dispatch_out *out, int32_t flags, void *stream) {
+  if (!x || !dst) return fail(MOE_ERR_INVALID, "moe_token_combine: NULL argument");
+  TokArgs a;
+  int st = fill_args(x, T, gates, out, flags, "moe_token_combine", &a);
+  if (st) return st;
+  moe_ctx *c = x->ctx;
+  for (int v = 0; v < c->n_local; ++v) {
+    if (!dst[v] && T > 0) return fail(MOE_ERR_INVALID, "moe_token_combine: NULL dst for local rank %d", v);
+    if ((uintptr_t)dst[v] & 15) return fail(MOE_ERR_INVALID, "moe_token_combine: dst must be 16-byte aligned");
+    a.dst[v] = (uint4 *)dst[v];
+  }
+  MOE_CUDA_TRY(cudaSetDevice(c->device));
+  const bool sync = c->rank >= 0 && c->G > 1;
+  a.epoch = sync ? ++x->arrive_epoch : 0;
+  k_tok_combine<<<x->blocks, kThreads, 0, (cudaStream_t)stream>>>(a);
+  MOE_CUDA_TRY(cudaGetLastError());
+  return MOE_OK;
+}

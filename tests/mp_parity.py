@@ -31,6 +31,8 @@ def main() -> int:
     ap.add_argument("--cf", type=float, default=0.0, help="capacity factor (row f2); 0 = none")
     ap.add_argument("--policy", type=int, default=0, help="0 alg1, 1 minmax, 2 static")
     ap.add_argument("--interval", type=int, default=1, help="re-placement interval (row f2)")
+    ap.add_argument("--tokens", type=int, default=-1,
+                    help="row f3: also run the token dispatch/combine with these flags (0 or 1)")
     args = ap.parse_args()
     rank, G, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -55,6 +57,30 @@ def main() -> int:
                                  dedup=args.dedup, capacity=cap, policy=args.policy,
                                  replan_interval=args.interval)
     layer.connect()
+    tx = None
+    if args.tokens >= 0:
+        from paper_2504_19925_b200 import TokenExchange
+        from oracle import dispatch as OD
+        from oracle import plan as OP
+        from oracle import tokens as OT
+        from oracle.numerics import f32_to_bf16_rne
+        trc = traces.make_trace(wl, iters=args.iters) if args.trace == "config" else \
+            traces.rotating_hot(E, wl.T, k, args.iters, seed=seed, hot_weight=4 if E < 16 else 16)
+        pl = OP.plan(np.ones(E, np.int64), E, G, S, {0: "alg1", 1: "minmax", 2: "static"}[args.policy])
+        rows = 1
+        for t, (ids, gates) in enumerate(trc):   # size the expert buffers from the oracle's loads
+            dd = OD.dispatch(traces.split_ranks(ids, G), traces.split_ranks(gates, G), pl["first_slot"], E, cap)
+            rows = max(rows, int(dd["slot_load"].max()))
+            if (t + 1) % args.interval == 0:
+                pl = OP.plan(dd["C"], E, G, S, {0: "alg1", 1: "minmax", 2: "static"}[args.policy])
+        tx = TokenExchange(layer.ctx, wl.d, rows)
+        tx.connect_process_group()
+
+        def bits(r, shape):
+            return f32_to_bf16_rne(r.normal(size=shape).astype(np.float32))
+
+        def dev(b):
+            return torch.from_numpy(b.view(np.int16).copy()).cuda().view(torch.bfloat16)
     if args.sampled:
         rng = np.random.default_rng(1)
         idx = np.unique(np.concatenate([rng.integers(0, P, 1024),
@@ -114,6 +140,30 @@ def main() -> int:
             expect(np.array_equal(got.view(np.uint32), np.ascontiguousarray(want[:, sel]).view(np.uint32)),
                    f"iter {t}: {nm}")
         check_weights(t)
+        if tx is not None:   # row f3 along this iteration's routing
+            from paper_2504_19925_b200 import api as A
+            r = np.random.default_rng([seed, t, 99])
+            xs = [bits(r, (Tg, wl.d)) for _ in range(G)]
+            use_gate = args.tokens & 1
+            gl = [traces.split_ranks(gates, G)[g].reshape(-1) for g in range(G)]
+            A.moe_token_dispatch(tx, [dev(xs[rank])], Tg, layer.out, gates=my_gates, flags=args.tokens)
+            layer.ctx.check()
+            want = np.zeros((G * S, tx.rows, wl.d), np.uint16)
+            for g in range(G):
+                OT.token_dispatch(xs[g], d["ranks"][g]["dest_slot"], d["ranks"][g]["dest_off"], want,
+                                  gates=gl[g] if use_gate else None)
+            got = tx.slot_view(0).view(torch.int16).cpu().numpy().view(np.uint16)
+            for ls in range(S):
+                n = int(d["slot_load"][rank * S + ls])
+                expect(np.array_equal(got[ls, :n], want[rank * S + ls, :n]), f"iter {t}: token rows slot {ls}")
+            y = bits(r, (G * S, tx.rows, wl.d))
+            tx.slot_view(0).copy_(dev(y[rank * S:(rank + 1) * S]).view(S, tx.rows, wl.d))
+            out_t = torch.empty(Tg * wl.d, dtype=torch.bfloat16, device="cuda")
+            A.moe_token_combine(tx, [out_t], Tg, layer.out, gates=my_gates, flags=args.tokens)
+            layer.ctx.check()
+            exp = OT.token_combine(y, rk["dest_slot"], rk["dest_off"], Tg, gates=gl[rank] if use_gate else None)
+            expect(np.array_equal(out_t.view(torch.int16).cpu().numpy().view(np.uint16).reshape(Tg, wl.d), exp),
+                   f"iter {t}: token combine")
     flag = torch.tensor([0 if ok else 1], device="cuda")
     dist.all_reduce(flag)
     if rank == 0:
@@ -121,6 +171,8 @@ def main() -> int:
               f"{'OK' if int(flag.item()) == 0 else 'FAIL'}", flush=True)
     if not ok:
         print(f"rank {rank}: " + "; ".join(msgs[:10]), flush=True)
+    if tx is not None:
+        tx.close()
     layer.close()
     dist.destroy_process_group()
     return int(flag.item() != 0)

@@ -23,7 +23,7 @@ def lib():
 
 def _declared():
     names = set()
-    for h in ("moe_dc.h", "moe_synth.h"):
+    for h in sorted(os.listdir(os.path.join(ROOT, "include"))):
         src = open(os.path.join(ROOT, "include", h)).read()
         src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
         names |= set(re.findall(r"\b(moe_[a-z_0-9]+)\s*\(", src))

@@ -1,0 +1,120 @@
+"""GPU parity of row f3 (token all-to-all, include/moe_tokens.h) against oracle/tokens.py:
+every written expert-buffer row and every combined token, bit for bit, over several
+iterations of a trace, with and without capacity drops and gate weighting."""
+import numpy as np
+import pytest
+import torch
+
+from synth import configs, traces
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    import __graft_entry__
+    __graft_entry__.build()
+    torch.cuda.set_device(0)
+
+
+def _bits(rng, shape):
+    """bf16 bit patterns of N(0, 1) values (inputs only; no method arithmetic)."""
+    from oracle.numerics import f32_to_bf16_rne
+    return f32_to_bf16_rne(rng.normal(size=shape).astype(np.float32))
+
+
+def _to_dev(bits: np.ndarray) -> torch.Tensor:
+    return torch.from_numpy(bits.view(np.int16).copy()).cuda().view(torch.bfloat16)
+
+
+def _from_dev(t: torch.Tensor) -> np.ndarray:
+    return t.view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+def run_tokens(name: str, G: int, iters: int, cf: float = 0.0, flags: int = 0, T: int | None = None):
+    from paper_2504_19925_b200 import DecoupledExpertLayer, TokenExchange, api
+    from oracle import dispatch as OD
+    from oracle import plan as OP
+    from oracle import tokens as OT
+    wl = configs.CONFIGS[name]
+    S, E, k, d = wl.S(G), wl.E, wl.k, wl.d
+    TT = wl.T if T is None else T
+    Tg = TT // G
+    cap = OD.slot_capacity(cf, TT, k, G * S) if cf > 0 else 0
+    tr = traces.make_trace(wl, iters=iters, T=TT)
+    # oracle routing for every iteration first (it sizes the buffers)
+    plan = OP.plan(np.ones(E, np.int64), E, G, S)
+    routes = []
+    for ids, gates in tr:
+        disp = OD.dispatch(traces.split_ranks(ids, G), traces.split_ranks(gates, G), plan["first_slot"], E, cap)
+        routes.append((plan, disp))
+        plan = OP.plan(disp["C"], E, G, S)
+    rows = max(1, max(int(dp["slot_load"].max()) for _, dp in routes))
+    layer = DecoupledExpertLayer(E, G, S, k, 8 * G, Tg, rank=-1, device=0, seed=1, capacity=cap)
+    tx = TokenExchange(layer.ctx, d, rows)
+    rng = np.random.default_rng(configs.seed_for(name) + 17)
+    use_gate = bool(flags & api.MOE_TOK_GATE)
+    for it, ((ids, gates), (plan_t, disp)) in enumerate(zip(tr, routes)):
+        layer.plan = api.Plan.from_first_slot(plan_t["first_slot"], G, S)
+        ids_d = torch.from_numpy(np.ascontiguousarray(ids)).cuda()
+        gates_d = torch.from_numpy(np.ascontiguousarray(gates)).cuda()
+        layer.dispatch(ids_d, gates_d, Tg)
+        xs = [_bits(rng, (Tg, d)) for _ in range(G)]
+        src = [_to_dev(x) for x in xs]
+        api.moe_token_dispatch(tx, src, Tg, layer.out, gates=gates_d, flags=flags)
+        layer.ctx.check()
+        want = np.zeros((G * S, rows, d), np.uint16)
+        for g in range(G):
+            rk = disp["ranks"][g]
+            OT.token_dispatch(xs[g], rk["dest_slot"], rk["dest_off"], want,
+                              gates=traces.split_ranks(gates, G)[g].reshape(-1) if use_gate else None)
+        for h in range(G):
+            got = _from_dev(tx.slot_view(h))
+            for ls in range(S):
+                n = int(disp["slot_load"][h * S + ls])
+                assert np.array_equal(got[ls, :n], want[h * S + ls, :n]), f"iter {it}: slot {h * S + ls} rows"
+        # the "expert": overwrite every buffer with synthetic outputs, then combine
+        y = _bits(rng, (G * S, rows, d))
+        for h in range(G):
+            tx.slot_view(h).copy_(_to_dev(y[h * S:(h + 1) * S]).view(S, rows, d))
+        dst = [torch.empty(Tg * d, dtype=torch.bfloat16, device="cuda") for _ in range(G)]
+        api.moe_token_combine(tx, dst, Tg, layer.out, gates=gates_d, flags=flags)
+        layer.ctx.check()
+        for g in range(G):
+            rk = disp["ranks"][g]
+            exp = OT.token_combine(y, rk["dest_slot"], rk["dest_off"], Tg,
+                                   gates=traces.split_ranks(gates, G)[g].reshape(-1) if use_gate else None)
+            assert np.array_equal(_from_dev(dst[g]).reshape(Tg, d), exp), f"iter {it} rank {g}: combine"
+    tx.close()
+    layer.close()
+
+
+@pytest.mark.parametrize("name,G,cf,flags", [("tiny-skew", 4, 0.0, 0), ("tiny-skew", 4, 0.0, 1),
+                                             ("tiny-odd", 3, 0.5, 1), ("tiny", 2, 1.0, 0),
+                                             ("medium", 4, 1.25, 1), ("medium", 1, 0.0, 0)])
+def test_token_dispatch_and_combine_virtual(name, G, cf, flags):
+    run_tokens(name, G, 3, cf=cf, flags=flags)
+
+
+def test_token_exchange_gpt_small_full_size():
+    """BASELINE's GPT-MoE small shape (d = 1024, T = 65 536, k = 2) at G = 1 and 8."""
+    run_tokens("gpt-small", 1, 1, flags=1)
+    run_tokens("gpt-small", 8, 1, cf=1.0, flags=0)
+
+
+def test_token_rows_overflow_raises():
+    from paper_2504_19925_b200 import DecoupledExpertLayer, MoeError, TokenExchange, api
+    layer = DecoupledExpertLayer(8, 1, 8, 2, 64, 128, rank=0, device=0)
+    ids = torch.stack([torch.zeros(128, dtype=torch.int32), torch.ones(128, dtype=torch.int32)], 1).cuda()
+    gates = torch.ones((128, 2), dtype=torch.float32, device="cuda")
+    layer.dispatch(ids, gates, 128)
+    tx = TokenExchange(layer.ctx, 16, 4)       # expert 0 alone gets 128 rows > 4
+    x = torch.zeros(128 * 16, dtype=torch.bfloat16, device="cuda")
+    api.moe_token_dispatch(tx, [x], 128, layer.out)
+    with pytest.raises(MoeError) as ei:
+        layer.ctx.check()
+    assert ei.value.status == 3
+    with pytest.raises(MoeError):
+        TokenExchange(layer.ctx, 12, 4)          # d % 8 != 0
+    tx.close()
+    layer.close()
