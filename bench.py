@@ -217,6 +217,82 @@ def _config(wl, G):
 
 
 # ------------------------------------------------------------------------------------------
+# Row f3: token all-to-all along the last iteration's routing
+# ------------------------------------------------------------------------------------------
+def token_a2a(args, wl, layer, G, rank, Tg, S, peak_hbm, barrier, stream):
+    """Times the forward pair -- moe_token_dispatch (plain copy) and moe_token_combine
+    (gate-weighted) -- on the
+    routing of the last timed iteration: bf16 activations [T_g][d] -> expert buffers ->
+    [T_g][d].  Algorithmic bytes per GPU: HBM = (T_g + rows landing in this
+    GPU's slots) * d * 2 per kernel; NVLink per direction = max(pairs this GPU sends to / pulls
+    from other GPUs, pairs other GPUs send to / pull from it) * d * 2."""
+    import torch
+    import torch.distributed as dist
+    from paper_2504_19925_b200 import TokenExchange, api
+    d = wl.d
+    out = layer.out
+    n = Tg * wl.k
+    ds = out.dest_slot[:n]
+    load = out.slot_load.to(torch.int64)
+    rows_t = load.max().reshape(1)
+    if G > 1:
+        dist.all_reduce(rows_t, op=dist.ReduceOp.MAX)
+    rows = max(1, int(rows_t.item()))
+    tx = TokenExchange(layer.ctx, d, rows)
+    tx.connect_process_group()
+    g = torch.Generator(device="cuda").manual_seed(1234 + rank)
+    src = torch.randn(Tg * d, device="cuda", generator=g).to(torch.bfloat16)
+    dst = torch.empty(Tg * d, dtype=torch.bfloat16, device="cuda")
+    gates = layer._last_gates
+    K = max(3, min(args.steps, 20))
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+    for _ in range(2):  # warm-up
+        api.moe_token_dispatch(tx, [src], Tg, out)
+        api.moe_token_combine(tx, [dst], Tg, out, gates=gates, flags=api.MOE_TOK_GATE)
+    barrier()
+    for i in range(K):  # back to back: rank skew is paid once, not per iteration
+        ev[i][0].record(stream)
+        api.moe_token_dispatch(tx, [src], Tg, out)
+        ev[i][1].record(stream)
+        api.moe_token_combine(tx, [dst], Tg, out, gates=gates, flags=api.MOE_TOK_GATE)
+        ev[i][2].record(stream)
+    barrier()
+    t_disp = sum(e[0].elapsed_time(e[1]) for e in ev[1:]) * K / (K - 1)
+    t_comb = sum(e[1].elapsed_time(e[2]) for e in ev[1:]) * K / (K - 1)
+    layer.ctx.check()
+    kept = ds >= 0
+    remote_out = int((kept & (ds // S != rank)).sum().item()) if G > 1 else 0
+    my_slots = load[rank * S:(rank + 1) * S] if G > 1 else load
+    rows_in = int(my_slots.sum().item())
+    own = int((kept & (ds // S == rank)).sum().item()) if G > 1 else rows_in
+    remote_in = rows_in - own
+    t = torch.tensor([t_disp / K, t_comb / K], device="cuda")
+    if G > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    disp_ms, comb_ms = (float(x) for x in t.tolist())
+    hbm = (Tg + rows_in) * d * 2
+    nvl = max(remote_out, remote_in) * d * 2
+    tx.close()
+
+    def roof(ms):
+        t_h = hbm / (peak_hbm * 1e9)
+        t_n = nvl / (GUIDE_NVLINK_GBS * 1e9)
+        if t_n > t_h:
+            ach = nvl / (ms * 1e-3) / 1e9
+            return {"bound": "nvlink", "achieved": round(ach, 1), "peak": GUIDE_NVLINK_GBS,
+                    "unit": "GB/s", "frac": round(ach / GUIDE_NVLINK_GBS, 4)}
+        ach = hbm / (ms * 1e-3) / 1e9
+        return {"bound": "hbm", "achieved": round(ach, 1), "peak": peak_hbm, "unit": "GB/s",
+                "frac": round(ach / peak_hbm, 4)}
+    return {"d": d, "rows_per_slot": rows, "steps": K,
+            "dispatch_ms": round(disp_ms, 4), "combine_ms": round(comb_ms, 4),
+            "hbm_bytes_per_kernel": hbm, "nvlink_bytes_per_kernel_per_dir": nvl,
+            "dispatch_roofline": roof(disp_ms), "combine_roofline": roof(comb_ms),
+            "note": "row f3 forward pair (copy dispatch, gate-weighted combine) on the last timed iteration's routing; "
+                    "rank 0's bytes, max-over-ranks times; not part of `value`"}
+
+
+# ------------------------------------------------------------------------------------------
 # GPU arm
 # ------------------------------------------------------------------------------------------
 def gpu_arm(args, wl):
@@ -268,6 +344,7 @@ def gpu_arm(args, wl):
         t = i % n_tr
         cur = layer.plan.first_slot.copy() if record else None
         nxt = layer.iterate(ids_d[t], gates_d[t], Tg)  # moe_step: a0+a2 -> a1 (host) -> a3+a4+a5
+        layer._last_gates = gates_d[t]
         if record:
             plans.append((cur, nxt.first_slot.copy()))
 
@@ -326,6 +403,7 @@ def gpu_arm(args, wl):
             gates_buf.copy_(gates_h[tt], non_blocking=True)
             layer.slot_g[0].copy_(grads_h, non_blocking=True)
             layer.iterate(ids_buf, gates_buf, Tg)       # counts come back to pinned host inside
+            layer._last_gates = gates_buf
         e2.record(stream)
         barrier()
         et = torch.tensor([s2.elapsed_time(e2) / Ke], device="cuda")
@@ -372,6 +450,8 @@ def gpu_arm(args, wl):
     t_roof_step = max((mean["stage_hbm"] + disp_hbm) / (peak_hbm * 1e9), t_nvl)
     launches_per_step = 3 + 1 + (2 if args.dedup else 0)
 
+    a2a = None if args.no_a2a else token_a2a(args, wl, layer, G, rank, Tg, S, peak_hbm, barrier, stream)
+
     cpu = None
     if rank == 0 and G == 1 and not args.no_cpu_baseline:
         ms, desc, _ = run_oracle_sample(wl, G, args.cpu_iters, frac_den=args.cpu_frac)
@@ -397,6 +477,7 @@ def gpu_arm(args, wl):
                                   "the 3 dispatch kernels; the update stage (= k_update_tma, or with "
                                   "de-dup k_presum + k_update_tma + k_replicate); max over ranks"},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * K,
+            "token_a2a": a2a,
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
@@ -423,6 +504,7 @@ def main():
                     help="placement policy (row f2: static = uniform baseline)")
     ap.add_argument("--interval", type=int, default=1, help="re-place every i iterations (row f2)")
     ap.add_argument("--cf", type=float, default=0.0, help="capacity factor; 0 = drop-free (row f2)")
+    ap.add_argument("--no-a2a", action="store_true", help="skip the row f3 token all-to-all timing")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-iters", type=int, default=3)
     ap.add_argument("--cpu-frac", type=int, default=64)

@@ -48,7 +48,8 @@ struct TokIpc {
   int64_t d, rows;
 };
 
-constexpr int kTokU = 4;  // 16-byte vectors per lane in flight
+constexpr int kTokU = 4;   // dispatch: 16-byte vectors per lane per row
+constexpr int kCombU = 2;  // combine: per row (two rows in flight -> 4 vectors per lane)
 
 }  // namespace
 
@@ -91,13 +92,11 @@ __device__ __forceinline__ void arrive_and_wait(const TokArgs &a) {
 __device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
 
-// fp32 -> bf16 RNE, NaN -> 0x7FFF (reading A17)
-__device__ __forceinline__ uint32_t rne16(float f) {
-  const uint32_t u = __float_as_uint(f);
-  if ((u & 0x7FFFFFFFu) > 0x7F800000u) return 0x7FFFu;
-  return (u + 0x7FFFu + ((u >> 16) & 1u)) >> 16;
+// fp32 pair -> packed bf16x2, RNE, NaN -> 0x7FFF (reading A17): one cvt.rn.bf16x2.f32
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+  const __nv_bfloat162 b = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t *>(&b);
 }
-__device__ __forceinline__ uint32_t pack2(float lo, float hi) { return rne16(lo) | (rne16(hi) << 16); }
 
 __device__ __forceinline__ uint4 scale8(uint4 v, float g) {
   uint4 r;
@@ -115,40 +114,66 @@ __device__ __forceinline__ uint4 ldg_nc(const uint4 *p) {
   return v;
 }
 
-__global__ void __launch_bounds__(kThreads) k_tok_dispatch(TokArgs a) {
+// Work item = (token, chunk of 32 x kTokU vectors of its row); a warp walks items with a
+// grid stride and loads item i+stride before storing item i (two rows in flight per warp).
+__device__ __forceinline__ void tok_item(const TokArgs &a, int64_t i, int64_t nch, int &v, int64_t &t,
+                                         int64_t &c0) {
+  // 32-bit division: n_local*T*k < 2^31 (moe_ctx_create) and nch <= d/8
+  const uint32_t tok = (uint32_t)i / (uint32_t)nch;
+  c0 = (int64_t)((uint32_t)i - tok * (uint32_t)nch) * (32 * kTokU);
+  v = (int)(tok / (uint32_t)a.T);
+  t = (int64_t)(tok - (uint32_t)v * (uint32_t)a.T);
+}
+
+__device__ __forceinline__ void tok_load(const TokArgs &a, int64_t i, int64_t nch, int lane, uint4 (&x)[kTokU]) {
+  int v;
+  int64_t t, c0;
+  tok_item(a, i, nch, v, t, c0);
+  const uint4 *src = a.src[v] + t * a.dv;
+#pragma unroll
+  for (int u = 0; u < kTokU; ++u) {
+    const int64_t c = c0 + u * 32 + lane;
+    if (c < a.dv) x[u] = ldg_nc(src + c);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 4) k_tok_dispatch(TokArgs a) {
   arrive_and_wait(a);
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (kThreads / 32);
-  const int64_t ntok = a.T * a.n_local;
-  for (int64_t w = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); w < ntok; w += warps) {
-    const int v = (int)(w / a.T);
-    const int64_t t = w - (int64_t)v * a.T;
+  const int64_t nch = (a.dv + 32 * kTokU - 1) / (32 * kTokU);
+  const int64_t nitems = a.T * a.n_local * nch;
+  int64_t i = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  uint4 x[kTokU];
+  if (i < nitems) tok_load(a, i, nch, lane, x);
+  while (i < nitems) {
+    const int64_t in = i + warps;
+    uint4 xn[kTokU];
+    if (in < nitems) tok_load(a, in, nch, lane, xn);
+    int v;
+    int64_t t, c0;
+    tok_item(a, i, nch, v, t, c0);
     const int64_t pbase = (int64_t)v * a.T * a.k + t * a.k;
-    const uint4 *src = a.src[v] + t * a.dv;
-    for (int64_t c0 = 0; c0 < a.dv; c0 += 32 * kTokU) {
-      uint4 x[kTokU];
+    for (int j = 0; j < a.k; ++j) {
+      const int s = __ldg(a.dest_slot + pbase + j);
+      if (s < 0) continue;  // dropped (reading B1)
+      const int off = __ldg(a.dest_off + pbase + j);
+      if (off >= a.rows) {
+        if (lane == 0 && c0 == 0) atomicOr(a.err, kErrData);
+        continue;
+      }
+      const uint32_t h = (uint32_t)s / (uint32_t)a.S;
+      uint4 *dst = a.xb[h] + ((int64_t)((uint32_t)s - h * (uint32_t)a.S) * a.rows + off) * a.dv;
+      const float g = a.gate ? __ldg(a.gates + pbase + j) : 1.f;
 #pragma unroll
       for (int u = 0; u < kTokU; ++u) {
         const int64_t c = c0 + u * 32 + lane;
-        if (c < a.dv) x[u] = ldg_nc(src + c);
-      }
-      for (int j = 0; j < a.k; ++j) {
-        const int s = __ldg(a.dest_slot + pbase + j);
-        if (s < 0) continue;  // dropped (reading B1)
-        const int off = __ldg(a.dest_off + pbase + j);
-        if (off >= a.rows) {
-          if (lane == 0 && c0 == 0) atomicOr(a.err, kErrData);
-          continue;
-        }
-        uint4 *dst = a.xb[s / a.S] + ((int64_t)(s % a.S) * a.rows + off) * a.dv;
-        const float g = a.gate ? __ldg(a.gates + pbase + j) : 1.f;
-#pragma unroll
-        for (int u = 0; u < kTokU; ++u) {
-          const int64_t c = c0 + u * 32 + lane;
-          if (c < a.dv) dst[c] = a.gate ? scale8(x[u], g) : x[u];
-        }
+        if (c < a.dv) dst[c] = a.gate ? scale8(x[u], g) : x[u];
       }
     }
+#pragma unroll
+    for (int u = 0; u < kTokU; ++u) x[u] = xn[u];
+    i = in;
   }
   if (a.rank >= 0 && a.G > 1) {  // barrier-out: the last CTA announces "my rows landed"
     __threadfence_system();
@@ -168,68 +193,92 @@ __global__ void k_tok_wait_done(TokSync *mine, int G, uint32_t epoch, int32_t *e
   if ((int)threadIdx.x < G) wait_flag(&mine->done[threadIdx.x], epoch, err);
 }
 
+__device__ __forceinline__ const uint4 *tok_row(const TokArgs &a, int64_t p, int lane, int c0, float &g,
+                                                bool &ok) {
+  const int s = __ldg(a.dest_slot + p);
+  ok = s >= 0;  // dropped pairs contribute nothing
+  if (!ok) return nullptr;
+  const int off = __ldg(a.dest_off + p);
+  if (off >= a.rows) {
+    if (lane == 0 && c0 == 0) atomicOr(a.err, kErrData);
+    ok = false;
+    return nullptr;
+  }
+  g = a.gate ? __ldg(a.gates + p) : 1.f;
+  const uint32_t h = (uint32_t)s / (uint32_t)a.S;
+  return a.xb[h] + ((int64_t)((uint32_t)s - h * (uint32_t)a.S) * a.rows + off) * a.dv;
+}
+
+__device__ __forceinline__ void tok_accum(const TokArgs &a, float (&acc)[kCombU][8], const uint4 (&y)[kCombU], float g) {
+#pragma unroll
+  for (int u = 0; u < kCombU; ++u) {
+    const uint32_t wd[4] = {y[u].x, y[u].y, y[u].z, y[u].w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float lo = bf_lo(wd[q]), hi = bf_hi(wd[q]);
+      if (a.gate) {
+        lo = __fmul_rn(g, lo);
+        hi = __fmul_rn(g, hi);
+      }
+      acc[u][2 * q] = __fadd_rn(acc[u][2 * q], lo);
+      acc[u][2 * q + 1] = __fadd_rn(acc[u][2 * q + 1], hi);
+    }
+  }
+}
+
+// One warp per (token, chunk) item; the k rows are loaded two at a time (both pairs' loads in
+// flight before either is accumulated), accumulation stays in ascending j (reading C2).
 __global__ void __launch_bounds__(kThreads) k_tok_combine(TokArgs a) {
   arrive_and_wait(a);
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (kThreads / 32);
-  const int64_t ntok = a.T * a.n_local;
-  for (int64_t w = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); w < ntok; w += warps) {
-    const int v = (int)(w / a.T);
-    const int64_t t = w - (int64_t)v * a.T;
+  const int64_t nch = (a.dv + 32 * kCombU - 1) / (32 * kCombU);
+  const int64_t nitems = a.T * a.n_local * nch;
+  for (int64_t i = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); i < nitems; i += warps) {
+    const uint32_t tok = (uint32_t)i / (uint32_t)nch;  // 32-bit: n_local*T*k < 2^31
+    const int64_t c0 = (int64_t)((uint32_t)i - tok * (uint32_t)nch) * (32 * kCombU);
+    const int v = (int)(tok / (uint32_t)a.T);
+    const int64_t t = (int64_t)(tok - (uint32_t)v * (uint32_t)a.T);
     const int64_t pbase = (int64_t)v * a.T * a.k + t * a.k;
-    uint4 *dst = a.dst[v] + t * a.dv;
-    for (int64_t c0 = 0; c0 < a.dv; c0 += 32 * kTokU) {
-      float acc[kTokU][8];
+    float acc[kCombU][8];
 #pragma unroll
-      for (int u = 0; u < kTokU; ++u)
+    for (int u = 0; u < kCombU; ++u)
 #pragma unroll
-        for (int i = 0; i < 8; ++i) acc[u][i] = 0.f;
-      for (int j = 0; j < a.k; ++j) {  // ascending j (reading C2)
-        const int s = __ldg(a.dest_slot + pbase + j);
-        if (s < 0) continue;
-        const int off = __ldg(a.dest_off + pbase + j);
-        if (off >= a.rows) {
-          if (lane == 0 && c0 == 0) atomicOr(a.err, kErrData);
-          continue;
-        }
-        const uint4 *row = a.xb[s / a.S] + ((int64_t)(s % a.S) * a.rows + off) * a.dv;
-        const float g = a.gate ? __ldg(a.gates + pbase + j) : 1.f;
-        uint4 y[kTokU];
+      for (int q = 0; q < 8; ++q) acc[u][q] = 0.f;
+    for (int j = 0; j < a.k; j += 2) {
+      float g0 = 1.f, g1 = 1.f;
+      bool ok0, ok1 = false;
+      const uint4 *r0 = tok_row(a, pbase + j, lane, (int)c0, g0, ok0);
+      const uint4 *r1 = (j + 1 < a.k) ? tok_row(a, pbase + j + 1, lane, (int)c0, g1, ok1) : nullptr;
+      uint4 y0[kCombU], y1[kCombU];
 #pragma unroll
-        for (int u = 0; u < kTokU; ++u) {
-          const int64_t c = c0 + u * 32 + lane;
-          if (c < a.dv) y[u] = ldg_nc(row + c);  // rows are final before the arrive flags
-        }
-#pragma unroll
-        for (int u = 0; u < kTokU; ++u) {
-          const uint32_t wd[4] = {y[u].x, y[u].y, y[u].z, y[u].w};
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            float lo = bf_lo(wd[q]), hi = bf_hi(wd[q]);
-            if (a.gate) {
-              lo = __fmul_rn(g, lo);
-              hi = __fmul_rn(g, hi);
-            }
-            acc[u][2 * q] = __fadd_rn(acc[u][2 * q], lo);
-            acc[u][2 * q + 1] = __fadd_rn(acc[u][2 * q + 1], hi);
-          }
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < kTokU; ++u) {
+      for (int u = 0; u < kCombU; ++u) {
         const int64_t c = c0 + u * 32 + lane;
-        if (c < a.dv) {
-          uint4 o;
-          o.x = pack2(acc[u][0], acc[u][1]);
-          o.y = pack2(acc[u][2], acc[u][3]);
-          o.z = pack2(acc[u][4], acc[u][5]);
-          o.w = pack2(acc[u][6], acc[u][7]);
-          dst[c] = o;
-        }
+        if (ok0 && c < a.dv) y0[u] = ldg_nc(r0 + c);  // rows are final before the arrive flags
+        if (ok1 && c < a.dv) y1[u] = ldg_nc(r1 + c);
+      }
+      if (ok0) tok_accum(a, acc, y0, g0);
+      if (ok1) tok_accum(a, acc, y1, g1);
+    }
+    uint4 *dst = a.dst[v] + t * a.dv;
+#pragma unroll
+    for (int u = 0; u < kCombU; ++u) {
+      const int64_t c = c0 + u * 32 + lane;
+      if (c < a.dv) {
+        uint4 o;
+        o.x = pack2(acc[u][0], acc[u][1]);
+        o.y = pack2(acc[u][2], acc[u][3]);
+        o.z = pack2(acc[u][4], acc[u][5]);
+        o.w = pack2(acc[u][6], acc[u][7]);
+        dst[c] = o;
       }
     }
   }
 }
+
+}  // namespace
+
+namespace {
 
 typedef int (*PFN_getAddressRange)(unsigned long long *, size_t *, unsigned long long);
 

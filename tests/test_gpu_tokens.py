@@ -118,3 +118,44 @@ def test_token_rows_overflow_raises():
         TokenExchange(layer.ctx, 12, 4)          # d % 8 != 0
     tx.close()
     layer.close()
+
+
+def test_special_values_bitwise():
+    """NaN payloads, +-Inf, denormals, signed zeros and fp32 rounding ties through the copy
+    dispatch (bits preserved) and the combine (fp32 sum -> bf16 RNE, NaN -> 0x7FFF, A17)."""
+    from paper_2504_19925_b200 import DecoupledExpertLayer, TokenExchange, api
+    from oracle import dispatch as OD
+    from oracle import plan as OP
+    from oracle import tokens as OT
+    E, G, S, k, T, d = 4, 1, 4, 2, 64, 64
+    rng = np.random.default_rng(3)
+    ids = np.stack([rng.permutation(E)[:k] for _ in range(T)]).astype(np.int32)
+    gates = rng.choice(np.array([1.0, 0.5, 3.0, 1e-30, -2.0, 1.0000001], np.float32), size=(T, k))
+    special = np.array([0x7FC0, 0xFFC1, 0x7F80, 0xFF80, 0x0001, 0x8001, 0x0000, 0x8000, 0x3F81, 0x7F7F,
+                        0x4B80, 0xCB80, 0x3F80, 0x0080], np.uint16)
+    x = rng.choice(special, size=(T, d)).astype(np.uint16)
+    plan = OP.plan(np.ones(E, np.int64), E, G, S)
+    disp = OD.dispatch([ids], [gates], plan["first_slot"], E)
+    rows = int(disp["slot_load"].max())
+    layer = DecoupledExpertLayer(E, G, S, k, 8, T, rank=0, device=0)
+    layer.plan = api.Plan.from_first_slot(plan["first_slot"], G, S)
+    gates_d = torch.from_numpy(gates).cuda()
+    layer.dispatch(torch.from_numpy(ids).cuda(), gates_d, T)
+    tx = TokenExchange(layer.ctx, d, rows)
+    for flags in (0, 1):
+        api.moe_token_dispatch(tx, [_to_dev(x)], T, layer.out, gates=gates_d, flags=flags)
+        want = np.zeros((S, rows, d), np.uint16)
+        OT.token_dispatch(x, disp["ranks"][0]["dest_slot"], disp["ranks"][0]["dest_off"], want,
+                          gates=gates.reshape(-1) if flags else None)
+        got = _from_dev(tx.slot_view(0))
+        for s in range(S):
+            n = int(disp["slot_load"][s])
+            assert np.array_equal(got[s, :n], want[s, :n]), (flags, s)
+        dst = torch.empty(T * d, dtype=torch.bfloat16, device="cuda")
+        api.moe_token_combine(tx, [dst], T, layer.out, gates=gates_d, flags=flags)
+        exp = OT.token_combine(want, disp["ranks"][0]["dest_slot"], disp["ranks"][0]["dest_off"], T,
+                               gates=gates.reshape(-1) if flags else None)
+        assert np.array_equal(_from_dev(dst).reshape(T, d), exp), flags
+    layer.ctx.check()
+    tx.close()
+    layer.close()
