@@ -93,7 +93,7 @@ class ClockSampler:
 
 
 def update_stage_bytes(fs_cur, fs_next, G: int, S: int, P: int, E: int, dedup: bool,
-                       parts: bool = False):
+                       parts: bool = False, host_state: bool = False):
     """Algorithmic bytes of one update stage, from the two plans.
 
     Returns (max over GPUs of HBM bytes, max over GPUs and directions of NVLink bytes); with
@@ -105,9 +105,11 @@ def update_stage_bytes(fs_cur, fs_next, G: int, S: int, P: int, E: int, dedup: b
     De-dup (row f1): a GPU with r >= 3 replicas of e first reads them (2rP) and writes an fp32
     partial (4P) that owners then read (4 B/element); a remote GPU receives each shard once
     and copies it into its other slots of e (read + write of the remote owners' ranges).
+    host_state (row f4): the 24 B/element of master/m/v cross PCIe instead (12 B each way),
+    reported as "pcie_per_dir"; the HBM bytes drop them.
     """
     Pg = P // G
-    upd = [24 * E * Pg] * G
+    upd = [0 if host_state else 24 * E * Pg] * G
     pre, rep = [0] * G, [0] * G
     nin, nout = [0] * G, [0] * G
     for e in range(E):
@@ -140,7 +142,7 @@ def update_stage_bytes(fs_cur, fs_next, G: int, S: int, P: int, E: int, dedup: b
     nvl = max(max(nin), max(nout))
     if parts:
         return {"stage_hbm": hbm, "nvl": nvl, "update_hbm": max(upd), "presum_hbm": max(pre),
-                "replicate_hbm": max(rep)}
+                "replicate_hbm": max(rep), "pcie_per_dir": 12 * E * Pg if host_state else 0}
     return hbm, nvl
 
 
@@ -214,6 +216,26 @@ def _config(wl, G):
             "T": wl.T, "G": G, "S": wl.S(G), "trace": wl.trace,
             "parallelism": f"decoupled-ep{G}",
             "l2": "inputs larger than L2 (optimizer state + slot grads/weights stream >126 MB per step)"}
+
+
+def measure_pcie(device: int, nbytes: int = 1 << 30) -> dict:
+    """Peak of the PCIe link as a copy engine sees it (pinned <-> device, best of 5)."""
+    import torch
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{device}")
+    out = {}
+    for name, dst, src in (("h2d_gbs", d, h), ("d2h_gbs", h, d)):
+        best = 1e9
+        for _ in range(5):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            dst.copy_(src, non_blocking=True)
+            b.record()
+            b.synchronize()
+            best = min(best, a.elapsed_time(b))
+        out[name] = nbytes / (best * 1e-3) / 1e9
+    del h, d
+    return out
 
 
 # ------------------------------------------------------------------------------------------
@@ -321,7 +343,8 @@ def gpu_arm(args, wl):
     cap = api.moe_slot_capacity(args.cf, wl.T, wl.k, G, S) if args.cf > 0 else 0
     layer = DecoupledExpertLayer(wl.E, G, S, wl.k, wl.P, Tg, rank=rank if G > 1 else 0,
                                  device=local, seed=seed, dedup=args.dedup, policy=pol,
-                                 capacity=cap, replan_interval=args.interval)
+                                 capacity=cap, replan_interval=args.interval,
+                                 host_state=args.host_state)
     if G > 1:
         layer.connect()
     n_tr = min(args.warmup + args.steps, args.trace_iters)
@@ -377,6 +400,8 @@ def gpu_arm(args, wl):
     pre_avg_local = tm["presum_ms"] / K
     rep_avg_local = tm["replicate_ms"] / K
     updk_avg_local = tm["update_kernel_ms"] / max(1, tm["n_update_kernel"])
+    if args.host_state:   # row f4: one step = several windowed launches + copies; time the stage
+        updk_avg_local = upd_avg_local
     t = torch.tensor([total_ms, upd_avg_local, disp_avg_local, pre_avg_local, rep_avg_local,
                       updk_avg_local], device="cuda")
     if G > 1:
@@ -424,13 +449,26 @@ def gpu_arm(args, wl):
         except Exception:
             args.traffic = None
     # algorithmic bytes, per timed iteration from the actual plans
-    acc = [update_stage_bytes(fc, fn, G, S, wl.P, wl.E, args.dedup, parts=True) for fc, fn in plans]
+    acc = [update_stage_bytes(fc, fn, G, S, wl.P, wl.E, args.dedup, parts=True,
+                              host_state=args.host_state) for fc, fn in plans]
     mean = {k: statistics.mean(a[k] for a in acc) for k in acc[0]}
     # roofline of the dominant kernel, k_update_tma alone (its own HBM and NVLink bytes)
     t_hbm_k = mean["update_hbm"] / (peak_hbm * 1e9)
     t_nvl = mean["nvl"] / (GUIDE_NVLINK_GBS * 1e9) if G > 1 else 0.0
     kname = "k_update_tma (fused reduce+Adam+place" + (", de-dup)" if args.dedup else ")")
-    if t_nvl > t_hbm_k:
+    pcie = measure_pcie(local) if args.host_state else None
+    t_pcie = mean["pcie_per_dir"] / (min(pcie["h2d_gbs"], pcie["d2h_gbs"]) * 1e9) if pcie else 0.0
+    if t_pcie > max(t_nvl, t_hbm_k):   # row f4: the state streams over PCIe
+        achieved = mean["pcie_per_dir"] / (updk_avg * 1e-3) / 1e9
+        pk = min(pcie["h2d_gbs"], pcie["d2h_gbs"])
+        roof = {"kernel": kname + " + copy-engine staging of the host-resident state", "bound": "pcie",
+                "achieved": round(achieved, 1), "peak": round(pk, 1), "unit": "GB/s",
+                "frac": round(achieved / pk, 4), "traffic": None,
+                "algorithmic_bytes_per_launch": int(mean["pcie_per_dir"]),
+                "peak_source": "measured in this run, all ranks at once: pinned<->device torch copies "
+                               f"of 1 GiB, H2D {pcie['h2d_gbs']:.1f} / D2H {pcie['d2h_gbs']:.1f} GB/s (min)",
+                "avg_launch_ms": round(updk_avg, 4)}
+    elif t_nvl > t_hbm_k:
         achieved = mean["nvl"] / (updk_avg * 1e-3) / 1e9
         roof = {"kernel": kname + ", NVLink pulls/pushes", "bound": "nvlink",
                 "achieved": round(achieved, 1), "peak": GUIDE_NVLINK_GBS, "unit": "GB/s",
@@ -447,8 +485,9 @@ def gpu_arm(args, wl):
                 "avg_launch_ms": round(updk_avg, 4)}
     disp_hbm = 28 * (wl.T // G) * wl.k
     # whole step: every HBM byte of dispatch + update stage at the HBM peak, or the NVLink bytes
-    t_roof_step = max((mean["stage_hbm"] + disp_hbm) / (peak_hbm * 1e9), t_nvl)
-    launches_per_step = 3 + 1 + (2 if args.dedup else 0)
+    t_roof_step = max((mean["stage_hbm"] + disp_hbm) / (peak_hbm * 1e9), t_nvl, t_pcie)
+    # our kernels launched in the timed region, from the library's own launch counters
+    n_launch = 3 * tm["n_dispatch"] + tm["n_update_kernel"] + tm["n_presum"] + tm["n_replicate"]
 
     a2a = None if args.no_a2a else token_a2a(args, wl, layer, G, rank, Tg, S, peak_hbm, barrier, stream)
 
@@ -463,12 +502,14 @@ def gpu_arm(args, wl):
             "steps": K, "warmup": args.warmup, "ms_per_step": round(ms_iter, 4),
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (walk-spike routing trace, counter-hash grads)",
-            "config": dict(_config(wl, G), dedup=bool(args.dedup), policy=args.policy,
+            "config": dict(_config(wl, G), dedup=bool(args.dedup), host_state=bool(args.host_state),
+                           policy=args.policy,
                            replan_interval=args.interval, capacity_factor=args.cf or None),
             "roofline": roof,
             "step_roofline": {"t_roof_ms": round(t_roof_step * 1e3, 4),
                               "frac": round(t_roof_step * 1e3 / ms_iter, 4),
-                              "basis": "max(HBM bytes of dispatch+update / peak HBM, NVLink bytes/dir / 770 GB/s)"},
+                              "basis": "max(HBM bytes of dispatch+update / peak HBM, NVLink bytes/dir / 770 GB/s"
+                                       + (", PCIe state bytes/dir / measured copy GB/s)" if pcie else ")")},
             "stages_ms": {"dispatch": round(disp_avg, 4), "update_stage": round(upd_avg, 4),
                           "update_kernel": round(updk_avg, 4),
                           "presum": round(pre_avg, 4), "replicate": round(rep_avg, 4),
@@ -476,7 +517,7 @@ def gpu_arm(args, wl):
                           "note": "library CUDA events (moe_ctx_set_timing) on the launching stream: "
                                   "the 3 dispatch kernels; the update stage (= k_update_tma, or with "
                                   "de-dup k_presum + k_update_tma + k_replicate); max over ranks"},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * K,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(n_launch),
             "token_a2a": a2a,
             "clocks": clocks,
         }
@@ -505,6 +546,8 @@ def main():
     ap.add_argument("--interval", type=int, default=1, help="re-place every i iterations (row f2)")
     ap.add_argument("--cf", type=float, default=0.0, help="capacity factor; 0 = drop-free (row f2)")
     ap.add_argument("--no-a2a", action="store_true", help="skip the row f3 token all-to-all timing")
+    ap.add_argument("--host-state", action="store_true",
+                    help="row f4: optimizer shards in pinned host memory (MOE_OPT_HOST_STATE)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-iters", type=int, default=3)
     ap.add_argument("--cpu-frac", type=int, default=64)

@@ -151,6 +151,15 @@ typedef struct {
  * Costs a library-owned fp32 buffer of min(E, S/3) x P per GPU.  Only useful when G > 1.  */
 #define MOE_OPT_DEDUP 1
 
+/* Row f4 (host-offloaded optimizer shards; PAPER.md:705, 734-736, 839-841 -- the paper's
+ * deployed design keeps the fp32 optimizer state in host DRAM): master/adam_m/adam_v are
+ * PINNED HOST memory (cudaHostAlloc / cudaHostRegister; with unified addressing the host
+ * pointer is device-accessible).  The same fused update kernel then streams the 12 B/param
+ * of state in and out over PCIe (zero-copy) while grads and weights stay in HBM; results are
+ * bit-identical.  moe_ctx_create fails with MOE_ERR_INVALID if the pointers are not pinned
+ * host memory (or, without the option, if they are not device memory).                */
+#define MOE_OPT_HOST_STATE 2
+
 /* Creates a context (allocates scratch and the sync buffer on desc->device).
  * Virtual mode is ready immediately.  Real mode (G > 1) additionally needs
  * moe_ctx_export + an exchange of the handles between ranks + moe_ctx_connect.  */

@@ -50,6 +50,7 @@ class MoeCtxDesc(C.Structure):
 
 
 MOE_OPT_DEDUP = 1
+MOE_OPT_HOST_STATE = 2
 
 
 class MoeDispatchOut(C.Structure):

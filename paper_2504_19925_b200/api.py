@@ -13,7 +13,7 @@ import numpy as np
 import torch
 
 from . import _lib as L
-from ._lib import (MOE_OPT_DEDUP, MOE_PLAN_KEEP, MOE_PLAN_MINMAX, MOE_PLAN_PAPER_ALG1,  # noqa: F401
+from ._lib import (MOE_OPT_DEDUP, MOE_OPT_HOST_STATE, MOE_PLAN_KEEP, MOE_PLAN_MINMAX, MOE_PLAN_PAPER_ALG1,  # noqa: F401
                    MOE_PLAN_STATIC, MoeError, check)
 
 
@@ -96,13 +96,20 @@ class MoeContext:
                  slot_w, slot_g, master, adam_m, adam_v, device: int | None = None,
                  options: int = 0):
         n_local = G if rank < 0 else 1
+        host = bool(options & MOE_OPT_HOST_STATE)
         for name, lst in (("slot_w", slot_w), ("slot_g", slot_g), ("master", master),
                           ("adam_m", adam_m), ("adam_v", adam_v)):
             if len(lst) != n_local:
                 raise ValueError(f"{name}: expected {n_local} tensors")
+            state = name in ("master", "adam_m", "adam_v")
             for t in lst:
-                if not (t.is_cuda and t.is_contiguous()):
-                    raise ValueError(f"{name}: tensors must be contiguous CUDA tensors")
+                if not t.is_contiguous():
+                    raise ValueError(f"{name}: tensors must be contiguous")
+                if state and host:
+                    if t.is_cuda or not t.is_pinned():
+                        raise ValueError(f"{name}: MOE_OPT_HOST_STATE needs pinned host tensors")
+                elif not t.is_cuda:
+                    raise ValueError(f"{name}: tensors must be CUDA tensors")
         for t in list(slot_w) + list(slot_g):
             if t.dtype != torch.bfloat16 or t.numel() != S * P:
                 raise ValueError("slot_w/slot_g: bf16 [S][P]")
@@ -112,6 +119,7 @@ class MoeContext:
         self.E, self.G, self.S, self.k, self.P = E, G, S, k, P
         self.rank, self.n_local, self.max_tokens = rank, n_local, max_tokens
         self.device = slot_w[0].device.index if device is None else device
+        self.host_state = host
         self._keep = (slot_w, slot_g, master, adam_m, adam_v)
 
         def arr(lst):

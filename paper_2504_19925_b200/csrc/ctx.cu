@@ -78,6 +78,16 @@ void free_ctx(moe_ctx *c) {
   cudaFree(c->item_ctr);
   cudaFree(c->scan_done);
   for (float *p : c->presum) cudaFree(p);
+  for (int b = 0; b < 3; ++b) {
+    cudaFree(c->hs_stage[b]);
+    if (c->hs_ev_in[b]) cudaEventDestroy(c->hs_ev_in[b]);
+    if (c->hs_ev_k[b]) cudaEventDestroy(c->hs_ev_k[b]);
+    if (c->hs_ev_out[b]) cudaEventDestroy(c->hs_ev_out[b]);
+  }
+  if (c->hs_ev_start) cudaEventDestroy(c->hs_ev_start);
+  if (c->hs_ev_end) cudaEventDestroy(c->hs_ev_end);
+  if (c->hs_in) cudaStreamDestroy(c->hs_in);
+  if (c->hs_out) cudaStreamDestroy(c->hs_out);
   if (c->host_flag) cudaFreeHost((void *)c->host_flag);
   for (auto *v : {&c->ev_pool, &c->ev_disp, &c->ev_upd, &c->ev_presum, &c->ev_repl, &c->ev_stage})
     for (auto &p : *v) {
@@ -116,8 +126,33 @@ extern "C" int moe_ctx_create(const moe_ctx_desc *d, moe_ctx **out) {
     if (al & 15) return fail(MOE_ERR_INVALID, "moe_ctx_create: buffers must be 16-byte aligned");
   }
   MOE_CUDA_TRY(cudaSetDevice(d->device));
+  const bool host_state = (d->options & MOE_OPT_HOST_STATE) != 0;
+  for (int v = 0; v < n_local; ++v) {  // the state must live where the option says
+    for (const void *p : {(const void *)d->master[v], (const void *)d->adam_m[v], (const void *)d->adam_v[v]}) {
+      cudaPointerAttributes at;
+      if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(MOE_ERR_INVALID, "moe_ctx_create: cannot query optimizer-state pointer %p", p);
+      }
+      if (host_state && at.type != cudaMemoryTypeHost)
+        return fail(MOE_ERR_INVALID, "moe_ctx_create: MOE_OPT_HOST_STATE needs pinned host master/m/v");
+      if (!host_state && at.type != cudaMemoryTypeDevice)
+        return fail(MOE_ERR_INVALID, "moe_ctx_create: master/m/v must be device memory "
+                                     "(or pass MOE_OPT_HOST_STATE for pinned host memory)");
+      if (host_state && at.devicePointer != p)
+        return fail(MOE_ERR_INVALID, "moe_ctx_create: host state must be device-accessible at the same address (UVA)");
+    }
+  }
 
   moe_ctx *c = new moe_ctx();
+  c->host_state = host_state;
+  c->hs_w = 0;
+  c->hs_in = c->hs_out = nullptr;
+  c->hs_ev_start = c->hs_ev_end = nullptr;
+  for (int b = 0; b < 3; ++b) {
+    c->hs_stage[b] = nullptr;
+    c->hs_ev_in[b] = c->hs_ev_k[b] = c->hs_ev_out[b] = nullptr;
+  }
   c->E = d->E;
   c->G = d->G;
   c->S = d->S;
@@ -199,6 +234,30 @@ extern "C" int moe_ctx_create(const moe_ctx_desc *d, moe_ctx **out) {
   {  // A/B switch for the update kernel: MOE_UPDATE_KERNEL=ldg selects the register-staged one
     const char *k = getenv("MOE_UPDATE_KERNEL");
     c->update_kernel = (k && std::string(k) == "ldg") ? 0 : 1;
+  }
+  if (c->host_state) {  // row f4: three staging windows of ~64 MB of state each, two copy streams
+    const int64_t pg_pad = (c->Pg + kChunk - 1) / kChunk * kChunk;
+    int64_t w = ((int64_t)64 << 20) / (12 * (int64_t)c->E * n_local) / kChunk * kChunk;
+    c->hs_w = std::min<int64_t>(pg_pad, std::max<int64_t>(kChunk, w));
+    cudaError_t he = cudaSuccess;
+    auto hchk = [&](cudaError_t x) {
+      if (x != cudaSuccess && he == cudaSuccess) he = x;
+    };
+    for (int b = 0; b < 3; ++b) {
+      hchk(cudaMalloc(&c->hs_stage[b], sizeof(float) * 3 * (size_t)n_local * c->E * c->hs_w));
+      hchk(cudaEventCreateWithFlags(&c->hs_ev_in[b], cudaEventDisableTiming));
+      hchk(cudaEventCreateWithFlags(&c->hs_ev_k[b], cudaEventDisableTiming));
+      hchk(cudaEventCreateWithFlags(&c->hs_ev_out[b], cudaEventDisableTiming));
+    }
+    hchk(cudaEventCreateWithFlags(&c->hs_ev_start, cudaEventDisableTiming));
+    hchk(cudaEventCreateWithFlags(&c->hs_ev_end, cudaEventDisableTiming));
+    hchk(cudaStreamCreateWithFlags(&c->hs_in, cudaStreamNonBlocking));
+    hchk(cudaStreamCreateWithFlags(&c->hs_out, cudaStreamNonBlocking));
+    if (he != cudaSuccess) {
+      cudaGetLastError();
+      free_ctx(c);
+      return fail(MOE_ERR_CUDA, "moe_ctx_create: host-state staging: %s", cudaGetErrorString(he));
+    }
   }
   // locality de-duplication: one fp32 partial-sum buffer per local GPU
   c->dedup = (d->options & MOE_OPT_DEDUP) && c->G > 1;

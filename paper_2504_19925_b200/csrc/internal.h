@@ -71,6 +71,14 @@ struct moe_ctx {
   moe::SyncBuf *peer_sync[MOE_MAX_G];
   float *peer_presum[MOE_MAX_G];  // fp32 [nq_max][P] local-replica partial sums (dedup)
 
+  // row f4: optimizer shards in pinned host memory (MOE_OPT_HOST_STATE), streamed through an
+  // HBM staging ring by the copy engines (window = hs_w elements of every expert)
+  bool host_state;
+  int64_t hs_w;                 // elements per window (multiple of kChunk)
+  float *hs_stage[3];           // [n_local][3 arrays][E][hs_w] each
+  cudaStream_t hs_in, hs_out;   // H2D / D2H copy streams
+  cudaEvent_t hs_ev_in[3], hs_ev_k[3], hs_ev_out[3], hs_ev_start, hs_ev_end;
+
   // locality de-duplication (MOE_OPT_DEDUP)
   bool dedup;
   int nq_max;                  // min(E, S / 3): partial-sum rows per GPU

@@ -31,6 +31,10 @@ namespace {
 struct UpdArgs {
   int32_t E, G, S, o_begin, o_count;
   int64_t P, Pg, nchunks;
+  // chunk window of this launch and the optimizer-state addressing: element loc of expert e
+  // is at state[o] + e * spitch + (loc - s_off).  Defaults: the whole range, [E][Pg] in place.
+  // Row f4 (host state) launches one window at a time on an HBM staging copy.
+  int64_t c_lo, c_cnt, spitch, s_off;
   float b1, omb1, b2, omb2, eps, step, rbc2, lrwd;
   int32_t wd_on;
   int32_t place_only;  // moe_place: skip a3/a4, place bf16(master) only
@@ -129,17 +133,17 @@ __device__ __forceinline__ void adam8(const UpdArgs &a, const float (&tot)[8], f
 }
 
 __global__ void __launch_bounds__(kThreads) k_update(const __grid_constant__ UpdArgs a) {
-  const int64_t per_owner = (int64_t)a.E * a.nchunks;
+  const int64_t per_owner = (int64_t)a.E * a.c_cnt;
   const int64_t total = per_owner * a.o_count;
   for (int64_t it = blockIdx.x; it < total; it += gridDim.x) {
     const int o = a.o_begin + (int)(it / per_owner);
     const int64_t rem = it - (int64_t)(o - a.o_begin) * per_owner;
     const int e = (int)(rem % a.E);  // chunk-major item order (see kItemOrder note)
-    const int64_t c = rem / a.E;
+    const int64_t c = a.c_lo + rem / a.E;
     const int64_t loc = c * kChunk + (int64_t)threadIdx.x * kVec;
     if (loc >= a.Pg) continue;
     const int64_t gi = (int64_t)o * a.Pg + loc;  // element index inside the expert
-    const int64_t so = (int64_t)e * a.Pg + loc;
+    const int64_t so = (int64_t)e * a.spitch + loc - a.s_off;
     if (a.place_only) {
       const float4 *pw = reinterpret_cast<const float4 *>(a.master[o] + so);
       const float4 x0 = pw[0], x1 = pw[1];
@@ -321,7 +325,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_update_tma(const __grid_cons
   }
   __syncthreads();
 
-  const int64_t per_owner = (int64_t)a.E * a.nchunks;
+  const int64_t per_owner = (int64_t)a.E * a.c_cnt;
   const int64_t total = per_owner * a.o_count;
   const int64_t P = a.P;
 
@@ -360,10 +364,10 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_update_tma(const __grid_cons
       const int o = a.o_begin + (int)(it / per_owner);
       const int64_t rem = it - (int64_t)(o - a.o_begin) * per_owner;
       const int e = (int)(rem % a.E);
-      const int64_t c = rem / a.E;
+      const int64_t c = a.c_lo + rem / a.E;
       const int64_t loc0 = c * kChunk;
       const uint32_t nval = (uint32_t)(a.Pg - loc0 < kChunk ? a.Pg - loc0 : kChunk);
-      const int64_t so = (int64_t)e * a.Pg + loc0;
+      const int64_t so = (int64_t)e * a.spitch + loc0 - a.s_off;
       {
         mbar_expect_tx(st_full + s, 3 * nval * 4);
         float *dst = state + (size_t)s * 3 * kChunk;
@@ -415,7 +419,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_update_tma(const __grid_cons
     const int o = a.o_begin + (int)(it / per_owner);
     const int64_t rem = it - (int64_t)(o - a.o_begin) * per_owner;
     const int e = (int)(rem % a.E);
-    const int64_t c = rem / a.E;
+    const int64_t c = a.c_lo + rem / a.E;
     const int64_t loc = c * kChunk + (int64_t)tid * kVec;
     const bool act = loc < a.Pg;
     float w[8], m[8], v[8];
@@ -496,7 +500,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_update_tma(const __grid_cons
     if (!act) continue;
     uint4 wb;
     adam8(a, tot, a.scale[e], w, m, v, wb);                              // a4
-    const int64_t so = (int64_t)e * a.Pg + loc;
+    const int64_t so = (int64_t)e * a.spitch + loc - a.s_off;
     float4 *pw = reinterpret_cast<float4 *>(a.master[o] + so);
     float4 *pm = reinterpret_cast<float4 *>(a.mom1[o] + so);
     float4 *pv = reinterpret_cast<float4 *>(a.mom2[o] + so);
@@ -685,6 +689,10 @@ int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *pl
   a.P = ctx->P;
   a.Pg = ctx->Pg;
   a.nchunks = (ctx->Pg + kChunk - 1) / kChunk;
+  a.c_lo = 0;
+  a.c_cnt = a.nchunks;
+  a.spitch = ctx->Pg;
+  a.s_off = 0;
   a.o_begin = ctx->rank >= 0 ? ctx->rank : 0;
   a.o_count = ctx->rank >= 0 ? 1 : ctx->G;
   a.place_only = place_only;
@@ -794,24 +802,86 @@ int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *pl
     k_barrier<<<1, 32, 0, s>>>(ba);
     MOE_CUDA_TRY(cudaGetLastError());
   }
-  const int64_t items = (int64_t)ctx->E * a.nchunks * a.o_count;
-  if (!tma) {
-    const int64_t grid = std::min<int64_t>(items, (int64_t)ctx->num_sms * ctx->upd_blocks_per_sm);
-    if (grid > 0) {
-      const auto tev = place_only ? std::pair<cudaEvent_t, cudaEvent_t>{nullptr, nullptr}
-                                  : timing_begin(ctx, s);
-      k_update<<<(unsigned)grid, kThreads, 0, s>>>(a);
-      MOE_CUDA_TRY(cudaGetLastError());
-      timing_end(ctx->ev_upd, tev, s);
+  // one launch of the fused kernel over a's chunk window
+  auto run_kernel = [&](UpdArgs &ka) -> int {
+    const int64_t items = (int64_t)ctx->E * ka.c_cnt * ka.o_count;
+    if (!tma) {
+      const int64_t grid = std::min<int64_t>(items, (int64_t)ctx->num_sms * ctx->upd_blocks_per_sm);
+      if (grid > 0) {
+        const auto tev = place_only ? std::pair<cudaEvent_t, cudaEvent_t>{nullptr, nullptr}
+                                    : timing_begin(ctx, s);
+        k_update<<<(unsigned)grid, kThreads, 0, s>>>(ka);
+        MOE_CUDA_TRY(cudaGetLastError());
+        timing_end(ctx->ev_upd, tev, s);
+      }
+    } else {
+      const int64_t grid = std::min<int64_t>(items, (int64_t)ctx->num_sms * 2);
+      if (grid > 0) {
+        const auto tev = timing_begin(ctx, s);
+        k_update_tma<<<(unsigned)grid, kTmaThreads, kTmaSmem, s>>>(ka);
+        MOE_CUDA_TRY(cudaGetLastError());
+        timing_end(ctx->ev_upd, tev, s);
+      }
     }
+    return MOE_OK;
+  };
+  if (!(ctx->host_state && !place_only)) {
+    const int st = run_kernel(a);
+    if (st) return st;
   } else {
-    const int64_t grid = std::min<int64_t>(items, (int64_t)ctx->num_sms * 2);
-    if (grid > 0) {
-      const auto tev = timing_begin(ctx, s);
-      k_update_tma<<<(unsigned)grid, kTmaThreads, kTmaSmem, s>>>(a);
-      MOE_CUDA_TRY(cudaGetLastError());
-      timing_end(ctx->ev_upd, tev, s);
+    // Row f4: the optimizer state lives in pinned host memory.  Windows of hs_w elements of
+    // every expert flow host -> HBM staging (copy engine, stream hs_in) -> fused kernel (s) ->
+    // host (copy engine, stream hs_out), three windows in flight: while the kernel updates
+    // window i, window i+1 is coming in and window i-1 going out, so PCIe runs both
+    // directions at once and the kernel sees HBM-resident state (bulk copies as usual).
+    if (!stage_ev.first) stage_ev = timing_begin(ctx, s);
+    const int64_t wc = ctx->hs_w / kChunk;
+    const int64_t nwin = (a.nchunks + wc - 1) / wc;
+    const int nl = ctx->n_local;
+    const int64_t EW = (int64_t)ctx->E * ctx->hs_w;
+    MOE_CUDA_TRY(cudaEventRecord(ctx->hs_ev_start, s));
+    MOE_CUDA_TRY(cudaStreamWaitEvent(ctx->hs_in, ctx->hs_ev_start, 0));
+    MOE_CUDA_TRY(cudaStreamWaitEvent(ctx->hs_out, ctx->hs_ev_start, 0));
+    for (int64_t wi = 0; wi < nwin; ++wi) {
+      const int b = (int)(wi % 3);
+      UpdArgs wa = a;
+      wa.c_lo = wi * wc;
+      wa.c_cnt = std::min<int64_t>(wc, a.nchunks - wa.c_lo);
+      const int64_t el0 = wa.c_lo * kChunk;
+      const int64_t eln = std::min<int64_t>(ctx->Pg, (wa.c_lo + wa.c_cnt) * kChunk) - el0;
+      wa.spitch = ctx->hs_w;
+      wa.s_off = el0;
+      if (wi >= 3) MOE_CUDA_TRY(cudaStreamWaitEvent(ctx->hs_in, ctx->hs_ev_out[b], 0));  // buffer b drained
+      for (int v = 0; v < nl; ++v) {
+        float *const host[3] = {ctx->master[v], ctx->adam_m[v], ctx->adam_v[v]};
+        for (int q = 0; q < 3; ++q) {
+          float *stg = ctx->hs_stage[b] + ((int64_t)v * 3 + q) * EW;
+          MOE_CUDA_TRY(cudaMemcpy2DAsync(stg, ctx->hs_w * 4, host[q] + el0, ctx->Pg * 4, eln * 4, ctx->E,
+                                         cudaMemcpyHostToDevice, ctx->hs_in));
+        }
+        wa.master[a.o_begin + v] = ctx->hs_stage[b] + ((int64_t)v * 3 + 0) * EW;
+        wa.mom1[a.o_begin + v] = ctx->hs_stage[b] + ((int64_t)v * 3 + 1) * EW;
+        wa.mom2[a.o_begin + v] = ctx->hs_stage[b] + ((int64_t)v * 3 + 2) * EW;
+      }
+      MOE_CUDA_TRY(cudaEventRecord(ctx->hs_ev_in[b], ctx->hs_in));
+      MOE_CUDA_TRY(cudaStreamWaitEvent(s, ctx->hs_ev_in[b], 0));
+      if (multi && tma) wa.epoch = (wi == 0) ? epoch : ++ctx->upd_epoch;  // fresh barriers per launch
+      const int st = run_kernel(wa);
+      if (st) return st;
+      MOE_CUDA_TRY(cudaEventRecord(ctx->hs_ev_k[b], s));
+      MOE_CUDA_TRY(cudaStreamWaitEvent(ctx->hs_out, ctx->hs_ev_k[b], 0));
+      for (int v = 0; v < nl; ++v) {
+        float *const host[3] = {ctx->master[v], ctx->adam_m[v], ctx->adam_v[v]};
+        for (int q = 0; q < 3; ++q) {
+          const float *stg = ctx->hs_stage[b] + ((int64_t)v * 3 + q) * EW;
+          MOE_CUDA_TRY(cudaMemcpy2DAsync(host[q] + el0, ctx->Pg * 4, stg, ctx->hs_w * 4, eln * 4, ctx->E,
+                                         cudaMemcpyDeviceToHost, ctx->hs_out));
+        }
+      }
+      MOE_CUDA_TRY(cudaEventRecord(ctx->hs_ev_out[b], ctx->hs_out));
     }
+    MOE_CUDA_TRY(cudaEventRecord(ctx->hs_ev_end, ctx->hs_out));  // the state is home again
+    MOE_CUDA_TRY(cudaStreamWaitEvent(s, ctx->hs_ev_end, 0));
   }
   if (multi && !tma) {  // barrier-out: every push into this GPU's slots has landed
     ba.which = 1;
@@ -843,8 +913,8 @@ int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *pl
       MOE_CUDA_TRY(cudaGetLastError());
       timing_end(ctx->ev_repl, rev, s);
     }
-    timing_end(ctx->ev_stage, stage_ev, s);
   }
+  timing_end(ctx->ev_stage, stage_ev, s);
   return MOE_OK;
 }
 

@@ -24,11 +24,12 @@ class DecoupledExpertLayer:
                  device: int | None = None, seed: int = 0, adam: api.AdamConfig | None = None,
                  policy: int = api.MOE_PLAN_PAPER_ALG1, scale_mode: int = 0, scale=None,
                  init_master: bool = True, dedup: bool = False, capacity: int = 0,
-                 replan_interval: int = 1):
+                 replan_interval: int = 1, host_state: bool = False):
         """capacity > 0 (per-replica slot capacity, see api.moe_slot_capacity) and
         replan_interval > 1 (re-place only every i iterations; MOE_PLAN_STATIC for the static
         baseline) are row f2 (readings B1-B3); the defaults are the paper's drop-free,
-        per-iteration path."""
+        per-iteration path.  host_state=True (row f4, MOE_OPT_HOST_STATE) keeps the fp32
+        master/m/v shards in pinned host memory; the update streams them over PCIe."""
         if replan_interval < 1:
             raise ValueError("replan_interval must be >= 1")
         self.replan_interval = replan_interval
@@ -46,12 +47,22 @@ class DecoupledExpertLayer:
         n = self.n_local
         self.slot_w = [torch.empty(S * P, dtype=torch.bfloat16, device=dev) for _ in range(n)]
         self.slot_g = [torch.zeros(S * P, dtype=torch.bfloat16, device=dev) for _ in range(n)]
-        self.master = [torch.empty(E * self.Pg, dtype=torch.float32, device=dev) for _ in range(n)]
-        self.adam_m = [torch.zeros(E * self.Pg, dtype=torch.float32, device=dev) for _ in range(n)]
-        self.adam_v = [torch.zeros(E * self.Pg, dtype=torch.float32, device=dev) for _ in range(n)]
+        if host_state:   # row f4: pinned host DRAM, device-accessible through UVA
+            def state(zero):
+                t = torch.empty(E * self.Pg, dtype=torch.float32, pin_memory=True)
+                return t.zero_() if zero else t
+        else:
+            def state(zero):
+                f = torch.zeros if zero else torch.empty
+                return f(E * self.Pg, dtype=torch.float32, device=dev)
+        self.master = [state(False) for _ in range(n)]
+        self.adam_m = [state(True) for _ in range(n)]
+        self.adam_v = [state(True) for _ in range(n)]
+        self.host_state = host_state
+        opts = (api.MOE_OPT_DEDUP if dedup else 0) | (api.MOE_OPT_HOST_STATE if host_state else 0)
         self.ctx = api.MoeContext(E, G, S, k, P, max_tokens, rank, self.slot_w, self.slot_g,
                                   self.master, self.adam_m, self.adam_v, device=device,
-                                  options=api.MOE_OPT_DEDUP if dedup else 0)
+                                  options=opts)
         self.dedup = dedup
         self.out = api.DispatchBuffers(self.ctx, max_tokens, capacity=capacity)
         self.seed = seed

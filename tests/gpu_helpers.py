@@ -16,7 +16,8 @@ def _u32(x: np.ndarray) -> np.ndarray:
 def run_parity(name: str, G: int, iters: int, *, rank_mode: str = "virtual", idx=None,
                T: int | None = None, policy: int = 0, scale_mode: int = 0, scale=None,
                weight_decay: float = 0.0, trace=None, check_dispatch: bool = True,
-               dedup: bool = False, capacity: int = 0, replan_interval: int = 1):
+               dedup: bool = False, capacity: int = 0, replan_interval: int = 1,
+               host_state: bool = False):
     """Returns the number of iterations compared.  rank_mode: "virtual" (rank=-1, G ranks on
     cuda:0) or "single" (real mode with G == 1)."""
     from paper_2504_19925_b200 import AdamConfig, DecoupledExpertLayer
@@ -37,7 +38,8 @@ def run_parity(name: str, G: int, iters: int, *, rank_mode: str = "virtual", idx
                       weight_decay=weight_decay)
     layer = DecoupledExpertLayer(E, G, S, k, P, Tg, rank=rank, device=0, seed=seed, adam=adam,
                                  policy=policy, scale_mode=scale_mode, scale=scale, dedup=dedup,
-                                 capacity=capacity, replan_interval=replan_interval)
+                                 capacity=capacity, replan_interval=replan_interval,
+                                 host_state=host_state)
     pol = {0: "alg1", 1: "minmax", 2: "static"}[policy]
     idx_arr = np.arange(P, dtype=np.int64) if idx is None else np.asarray(idx, dtype=np.int64)
     sim = ostep.OracleSim(E, G, S, P, seed, hyper=hyper, policy=pol, scale_mode=scale_mode,
@@ -92,7 +94,7 @@ def run_parity(name: str, G: int, iters: int, *, rank_mode: str = "virtual", idx
             cols = sel.cpu().numpy()
             for name_, arr, want in (("master", layer.master, sim.master), ("m", layer.adam_m, sim.m),
                                      ("v", layer.adam_v, sim.v)):
-                got = arr[v].view(E, Pg)[:, li].cpu().numpy()
+                got = arr[v].view(E, Pg)[:, li.to(arr[v].device)].cpu().numpy()
                 assert np.array_equal(_u32(got), _u32(want[:, cols])), f"iter {t} owner {v}: {name_}"
         _compare_weights(layer, sim, idx_t, G, S, P, t)
     layer.close()

@@ -31,6 +31,7 @@ def main() -> int:
     ap.add_argument("--cf", type=float, default=0.0, help="capacity factor (row f2); 0 = none")
     ap.add_argument("--policy", type=int, default=0, help="0 alg1, 1 minmax, 2 static")
     ap.add_argument("--interval", type=int, default=1, help="re-placement interval (row f2)")
+    ap.add_argument("--host-state", action="store_true", help="row f4: state in pinned host memory")
     ap.add_argument("--tokens", type=int, default=-1,
                     help="row f3: also run the token dispatch/combine with these flags (0 or 1)")
     args = ap.parse_args()
@@ -55,7 +56,7 @@ def main() -> int:
     cap = slot_capacity(args.cf, wl.T, k, G * S) if args.cf > 0 else 0
     layer = DecoupledExpertLayer(E, G, S, k, P, Tg, rank=rank, device=local, seed=seed,
                                  dedup=args.dedup, capacity=cap, policy=args.policy,
-                                 replan_interval=args.interval)
+                                 replan_interval=args.interval, host_state=args.host_state)
     layer.connect()
     tx = None
     if args.tokens >= 0:
@@ -133,7 +134,9 @@ def main() -> int:
         expect(np.array_equal(layer.out.send_gate.cpu().numpy()[:nk].view(np.uint32),
                               rk["send_gate"].view(np.uint32)), f"iter {t}: send_gate")
         sel = (idx >= rank * Pg) & (idx < (rank + 1) * Pg)
-        li = torch.from_numpy(idx[sel] - rank * Pg).cuda()
+        li = torch.from_numpy(idx[sel] - rank * Pg)
+        if not args.host_state:
+            li = li.cuda()
         for nm, arr, want in (("master", layer.master, sim.master), ("m", layer.adam_m, sim.m),
                               ("v", layer.adam_v, sim.v)):
             got = arr[0].view(E, Pg)[:, li].cpu().numpy()

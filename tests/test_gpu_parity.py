@@ -233,3 +233,27 @@ def test_policy_drops_long_horizon(policy, interval):
     from policy_study import run
     r = run(1, 150, policy, interval)
     assert r["pairs"] == 150 * 4096 * 2
+
+
+@pytest.mark.parametrize("name,G,dedup", [("medium", 1, False), ("medium", 4, True), ("tiny-odd", 3, False)])
+def test_host_state_is_bit_identical(name, G, dedup):
+    """Row f4: fp32 master/m/v in pinned host memory (MOE_OPT_HOST_STATE), streamed over PCIe by
+    the same fused update kernel -- bitwise the oracle, every element, every iteration."""
+    from gpu_helpers import run_parity
+    run_parity(name, G, 4, host_state=True, dedup=dedup)
+
+
+def test_host_state_pointer_checks():
+    """moe_ctx_create checks the state's memory type against MOE_OPT_HOST_STATE (C level)."""
+    import ctypes as C
+    from paper_2504_19925_b200 import DecoupledExpertLayer, _lib as L
+    for host in (False, True):
+        lay = DecoupledExpertLayer(8, 1, 8, 2, 64, 16, rank=0, device=0, host_state=host)
+        arrs = [(C.c_void_p * 1)(t[0].data_ptr()) for t in
+                (lay.slot_w, lay.slot_g, lay.master, lay.adam_m, lay.adam_v)]
+        wrong = 0 if host else L.MOE_OPT_HOST_STATE          # the opposite of the truth
+        desc = L.MoeCtxDesc(8, 1, 8, 2, 64, 16, 0, 0, *[C.cast(a, C.POINTER(C.c_void_p)) for a in arrs], wrong)
+        h = C.c_void_p()
+        assert L.lib().moe_ctx_create(C.byref(desc), C.byref(h)) == 1
+        assert b"host" in L.lib().moe_last_error()
+        lay.close()
