@@ -78,6 +78,9 @@ void free_ctx(moe_ctx *c) {
   cudaFree(c->item_ctr);
   cudaFree(c->scan_done);
   for (float *p : c->presum) cudaFree(p);
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->ev_side_start) cudaEventDestroy(c->ev_side_start);
+  if (c->ev_presum_done) cudaEventDestroy(c->ev_presum_done);
   for (int b = 0; b < 3; ++b) {
     cudaFree(c->hs_stage[b]);
     if (c->hs_ev_in[b]) cudaEventDestroy(c->hs_ev_in[b]);
@@ -272,6 +275,14 @@ extern "C" int moe_ctx_create(const moe_ctx_desc *d, moe_ctx **out) {
         return fail(MOE_ERR_CUDA, "moe_ctx_create: cannot allocate the de-duplication buffer");
       }
       c->presum.push_back(p);
+    }
+    cudaError_t se = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
+    if (se == cudaSuccess) se = cudaEventCreateWithFlags(&c->ev_side_start, cudaEventDisableTiming);
+    if (se == cudaSuccess) se = cudaEventCreateWithFlags(&c->ev_presum_done, cudaEventDisableTiming);
+    if (se != cudaSuccess) {
+      cudaGetLastError();
+      free_ctx(c);
+      return fail(MOE_ERR_CUDA, "moe_ctx_create: side stream: %s", cudaGetErrorString(se));
     }
   }
   for (int h = 0; h < MOE_MAX_G; ++h) {

@@ -83,6 +83,10 @@ struct moe_ctx {
   bool dedup;
   int nq_max;                  // min(E, S / 3): partial-sum rows per GPU
   std::vector<float *> presum; // [n_local] library-owned
+  cudaStream_t side;           // low-priority stream for the early k_presum (moe_step)
+  cudaEvent_t ev_side_start, ev_presum_done;
+  bool presum_ready;           // a k_presum for plan presum_fs is in flight on `side`
+  std::vector<int32_t> presum_fs;
 
   // library-owned device scratch
   moe::SyncBuf *sync;       // this GPU's sync buffer (virtual mode: the single shared one)

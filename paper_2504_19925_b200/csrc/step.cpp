@@ -13,10 +13,14 @@ extern "C" int moe_step(moe_ctx *ctx, const int32_t *topk_ids, const float *gate
   if (!ctx || !out || !plan_cur || !plan_next || !adam)
     return moe::fail(MOE_ERR_INVALID, "moe_step: NULL argument");
   if (!out->counts_host) return moe::fail(MOE_ERR_INVALID, "moe_step: out->counts_host is required");
-  int st = moe_dispatch(ctx, topk_ids, gates, T, plan_cur, out, stream);  // a0 + a2
+  // de-dup partials (a3's first level) need only plan_t and the grads: start them now on a
+  // low-priority side stream, overlapping the dispatch and the host planner
+  int st = moe_presum_prelaunch(ctx, plan_cur, stream);
   if (st) return st;
+  st = moe_dispatch(ctx, topk_ids, gates, T, plan_cur, out, stream);  // a0 + a2
+  if (st) return moe_step_abort(ctx, st);
   st = moe_ctx_wait_counts(ctx);  // C_t on the host
-  if (st) return st;
+  if (st) return moe_step_abort(ctx, st);
   if (policy == MOE_PLAN_KEEP) {  // interval policy between re-plans: plan_{t+1} = plan_t
     if (!plan_next->replicas || !plan_next->first_slot || !plan_next->slot_expert || !plan_cur->replicas ||
         !plan_cur->slot_expert)
@@ -31,7 +35,7 @@ extern "C" int moe_step(moe_ctx *ctx, const int32_t *topk_ids, const float *gate
   } else {
     st = moe_plan_ex(out->counts_host, plan_cur->E, plan_cur->G, plan_cur->S, policy, plan_next,
                      nullptr);  // a1 -> plan_{t+1}
-    if (st) return st;
+    if (st) return moe_step_abort(ctx, st);
   }
   return moe_update(ctx, plan_cur, plan_next, adam, stream);  // a3 + a4 + a5
 }

@@ -674,6 +674,40 @@ int moe_update_init() {
 
 namespace {
 
+// De-dup partial rows under plan_cur: for each GPU h, the experts with >= 3 replicas on h, in
+// ascending order (row q of h's presum buffer); pq[e][h] = q or -1.
+int build_presum(moe_ctx *ctx, const moe_plan_t *plan_cur, int8_t (&pq)[MOE_MAX_E][MOE_MAX_G], PresumArgs &pa) {
+  const int o_begin = ctx->rank >= 0 ? ctx->rank : 0;
+  memset(pq, -1, sizeof(pq));
+  pa = PresumArgs{};
+  pa.S = ctx->S;
+  pa.o_begin = o_begin;
+  pa.P = ctx->P;
+  pa.nchunks = (ctx->P + kChunk - 1) / kChunk;
+  for (int e = 0; e <= ctx->E; ++e) pa.fs[e] = plan_cur->first_slot[e];
+  for (int h = 0; h < ctx->G; ++h) {
+    int nq = 0;
+    for (int e = 0; e < ctx->E; ++e) {
+      const int ja = std::max(pa.fs[e], h * ctx->S), jb = std::min(pa.fs[e + 1], (h + 1) * ctx->S);
+      if (jb - ja >= 3) {
+        pq[e][h] = (int8_t)nq;
+        const int v = h - o_begin;
+        if (v >= 0 && v < ctx->n_local) pa.q_e[v][nq] = (int16_t)e;
+        ++nq;
+      }
+    }
+    if (nq > ctx->nq_max) return fail(MOE_ERR_INTERNAL, "de-dup: %d partial rows > %d", nq, ctx->nq_max);
+    const int v = h - o_begin;
+    if (v >= 0 && v < ctx->n_local) pa.qoff[v + 1] = pa.qoff[v] + nq;
+  }
+  pa.nq_total = pa.qoff[ctx->n_local];
+  for (int v = 0; v < ctx->n_local; ++v) {
+    pa.grads[v] = (const uint16_t *)ctx->slot_g[v];
+    pa.presum[v] = ctx->presum[v];
+  }
+  return MOE_OK;
+}
+
 // Shared launcher of moe_update (place_only = 0) and moe_place (place_only = 1).
 int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *plan_next,
                   const moe_adam_t *adam, int place_only, void *stream) {
@@ -749,40 +783,22 @@ int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *pl
   memset(a.pq, -1, sizeof(a.pq));
   PresumArgs pa{};
   if (dedup) {  // partial rows: for each GPU h, experts with >= 3 replicas on h, ascending
-    pa.S = ctx->S;
-    pa.o_begin = a.o_begin;
-    pa.P = ctx->P;
-    pa.nchunks = (ctx->P + kChunk - 1) / kChunk;
-    for (int e = 0; e <= ctx->E; ++e) pa.fs[e] = plan_cur->first_slot[e];
-    for (int h = 0; h < ctx->G; ++h) {
-      int nq = 0;
-      for (int e = 0; e < ctx->E; ++e) {
-        const int ja = std::max(pa.fs[e], h * ctx->S), jb = std::min(pa.fs[e + 1], (h + 1) * ctx->S);
-        if (jb - ja >= 3) {
-          a.pq[e][h] = (int8_t)nq;
-          const int v = h - a.o_begin;
-          if (v >= 0 && v < ctx->n_local) pa.q_e[v][nq] = (int16_t)e;
-          ++nq;
-        }
-      }
-      if (nq > ctx->nq_max) return fail(MOE_ERR_INTERNAL, "de-dup: %d partial rows > %d", nq, ctx->nq_max);
-      const int v = h - a.o_begin;
-      if (v >= 0 && v < ctx->n_local) pa.qoff[v + 1] = pa.qoff[v] + nq;
-    }
-    pa.nq_total = pa.qoff[ctx->n_local];
-    for (int v = 0; v < ctx->n_local; ++v) {
-      pa.grads[v] = (const uint16_t *)ctx->slot_g[v];
-      pa.presum[v] = ctx->presum[v];
-    }
+    const int st = build_presum(ctx, plan_cur, a.pq, pa);
+    if (st) return st;
     for (int h = 0; h < ctx->G; ++h) a.presum[h] = ctx->peer_presum[h];
     stage_ev = timing_begin(ctx, s);  // with de-dup the timed "update" is the whole stage
-    if (pa.nq_total > 0) {
+    bool pre = ctx->presum_ready;     // moe_step launched it early on the side stream?
+    for (int e = 0; pre && e <= ctx->E; ++e) pre = ctx->presum_fs[e] == plan_cur->first_slot[e];
+    if (pre) {
+      MOE_CUDA_TRY(cudaStreamWaitEvent(s, ctx->ev_presum_done, 0));
+    } else if (pa.nq_total > 0) {
       const int64_t grid = std::min<int64_t>((int64_t)pa.nq_total * pa.nchunks, (int64_t)ctx->num_sms * 8);
       const auto pev = timing_begin(ctx, s);
       k_presum<<<(unsigned)grid, kThreads, 0, s>>>(pa);
       MOE_CUDA_TRY(cudaGetLastError());
       timing_end(ctx->ev_presum, pev, s);
     }
+    ctx->presum_ready = false;
   }
   a.fused_barrier = (multi && tma) ? 1 : 0;  // k_update_tma carries both barriers itself
   a.rank = ctx->rank;
@@ -931,6 +947,42 @@ extern "C" int moe_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_pl
   if (adam->scale_mode < 0 || adam->scale_mode > 2 || (adam->scale_mode == 2 && !adam->scale))
     return fail(MOE_ERR_INVALID, "moe_update: bad scale_mode / scale");
   return launch_update(ctx, plan_cur, plan_next, adam, 0, stream);
+}
+
+// moe_step's early start of the de-dup partial sums (they need only plan_t and the grads, both
+// ready when the step begins): k_presum on the context's side stream with a persistent grid of
+// 2 CTAs per SM (a quarter of the thread slots, ~64 KB of loads in flight per SM), so the
+// dispatch kernels -- the host planner's critical path -- co-reside instead of queueing
+// behind it.  moe_update then waits on its event instead of launching it.
+int moe_presum_prelaunch(moe_ctx *ctx, const moe_plan_t *plan_cur, void *stream) {
+  ctx->presum_ready = false;
+  if (!ctx->dedup) return MOE_OK;
+  int st = moe_validate_plan(ctx, plan_cur, "moe_step(plan_cur)");
+  if (st) return st;
+  MOE_CUDA_TRY(cudaSetDevice(ctx->device));
+  int8_t pq[MOE_MAX_E][MOE_MAX_G];
+  PresumArgs pa{};
+  st = build_presum(ctx, plan_cur, pq, pa);
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  MOE_CUDA_TRY(cudaEventRecord(ctx->ev_side_start, s));
+  MOE_CUDA_TRY(cudaStreamWaitEvent(ctx->side, ctx->ev_side_start, 0));
+  if (pa.nq_total > 0) {
+    const int64_t grid = std::min<int64_t>((int64_t)pa.nq_total * pa.nchunks, (int64_t)ctx->num_sms * 2);
+    const auto pev = timing_begin(ctx, ctx->side);
+    k_presum<<<(unsigned)grid, kThreads, 0, ctx->side>>>(pa);
+    MOE_CUDA_TRY(cudaGetLastError());
+    timing_end(ctx->ev_presum, pev, ctx->side);
+  }
+  MOE_CUDA_TRY(cudaEventRecord(ctx->ev_presum_done, ctx->side));
+  ctx->presum_fs.assign(plan_cur->first_slot, plan_cur->first_slot + ctx->E + 1);
+  ctx->presum_ready = true;
+  return MOE_OK;
+}
+
+int moe_step_abort(moe_ctx *ctx, int status) {
+  ctx->presum_ready = false;
+  return status;
 }
 
 extern "C" int moe_place(moe_ctx *ctx, const moe_plan_t *plan, void *stream) {
