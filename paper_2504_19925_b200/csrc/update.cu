@@ -60,6 +60,10 @@ struct UpdArgs {
   int32_t dedup;
   int8_t pq[MOE_MAX_E][MOE_MAX_G];  // row of expert e's fp32 partial on GPU h under plan_cur, or -1
   const float *presum[MOE_MAX_G];   // per GPU h: fp32 [nq_max][P]
+  // development trace (env MOE_KTRACE): globaltimer stamps folded with atomics, printed by the
+  // CTA that completes barrier-out.  [0] min start [1] max start [2] max barrier-in done
+  // [3] min consumer done [4] max consumer done
+  unsigned long long *ktrace;
 };
 
 __device__ __forceinline__ uint4 ld_stream(const uint16_t *p) {
@@ -328,6 +332,11 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_update_tma(const __grid_cons
   const int64_t per_owner = (int64_t)a.E * a.c_cnt;
   const int64_t total = per_owner * a.o_count;
   const int64_t P = a.P;
+  if (a.ktrace && threadIdx.x == 0) {
+    const unsigned long long t = globaltimer();
+    atomicMin(a.ktrace + 0, t);
+    atomicMax(a.ktrace + 1, t);
+  }
 
   // Barrier-in (real mode): "every GPU's slot grads are ready".  This GPU's earlier stream
   // work (the backward that wrote its grads) is complete when this kernel starts; one thread
@@ -342,6 +351,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_update_tma(const __grid_cons
     if (lane != 0) return;
     if (a.fused_barrier)
       for (int h = 0; h < a.G; ++h) wait_flag(&a.sync_local->upd_in[h], a.epoch, a.err);
+    if (a.ktrace) atomicMax(a.ktrace + 2, globaltimer());
     uint32_t si = 0, gi_ = 0;
     for (;;) {
       // dynamic scheduling: claim the next item (chunk-major order, see kItemOrder note)
@@ -517,6 +527,11 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_update_tma(const __grid_cons
   // fences its own (peer) stores at system scope; the consumer warps meet on a named barrier;
   // the last CTA of this GPU signals every peer and waits for all of them, so this kernel ends
   // only after all weights of plan_next are in place on this GPU.
+  if (a.ktrace && tid == 0) {
+    const unsigned long long t = globaltimer();
+    atomicMin(a.ktrace + 3, t);
+    atomicMax(a.ktrace + 4, t);
+  }
   if (a.fused_barrier) {
     __threadfence_system();
     asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory");
@@ -525,6 +540,13 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_update_tma(const __grid_cons
       __threadfence_system();
       for (int h = 0; h < a.G; ++h) st_release_sys(&a.sync_peer[h]->upd_out[a.rank], a.epoch);
       for (int h = 0; h < a.G; ++h) wait_flag(&a.sync_local->upd_out[h], a.epoch, a.err);
+      if (a.ktrace) {
+        const unsigned long long *k = a.ktrace, t = globaltimer();
+        printf("KTRACE rank %d epoch %u: start spread %.1f us | barrier-in done +%.1f | consumers done "
+               "+%.1f .. +%.1f | barrier-out done +%.1f us\n",
+               a.rank, a.epoch, (k[1] - k[0]) * 1e-3, (k[2] - k[0]) * 1e-3, (k[3] - k[0]) * 1e-3,
+               (k[4] - k[0]) * 1e-3, (t - k[0]) * 1e-3);
+      }
     }
   }
 }
@@ -818,8 +840,17 @@ int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *pl
     k_barrier<<<1, 32, 0, s>>>(ba);
     MOE_CUDA_TRY(cudaGetLastError());
   }
+  static const bool ktrace_on = getenv("MOE_KTRACE") != nullptr;
+  static unsigned long long *ktrace_buf = nullptr;
+  if (ktrace_on && tma && !ktrace_buf) MOE_CUDA_TRY(cudaMalloc(&ktrace_buf, 8 * sizeof(unsigned long long)));
   // one launch of the fused kernel over a's chunk window
   auto run_kernel = [&](UpdArgs &ka) -> int {
+    ka.ktrace = nullptr;
+    if (ktrace_on && tma) {
+      unsigned long long init[8] = {~0ull, 0, 0, ~0ull, 0, 0, 0, 0};
+      MOE_CUDA_TRY(cudaMemcpyAsync(ktrace_buf, init, sizeof(init), cudaMemcpyHostToDevice, s));
+      ka.ktrace = ktrace_buf;
+    }
     const int64_t items = (int64_t)ctx->E * ka.c_cnt * ka.o_count;
     if (!tma) {
       const int64_t grid = std::min<int64_t>(items, (int64_t)ctx->num_sms * ctx->upd_blocks_per_sm);
