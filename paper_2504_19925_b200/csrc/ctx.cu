@@ -79,6 +79,9 @@ void free_ctx(moe_ctx *c) {
   cudaFree(c->scan_done);
   for (float *p : c->presum) cudaFree(p);
   if (c->side) cudaStreamDestroy(c->side);
+  if (c->hi) cudaStreamDestroy(c->hi);
+  if (c->ev_hi_in) cudaEventDestroy(c->ev_hi_in);
+  if (c->ev_hi_out) cudaEventDestroy(c->ev_hi_out);
   if (c->ev_side_start) cudaEventDestroy(c->ev_side_start);
   if (c->ev_presum_done) cudaEventDestroy(c->ev_presum_done);
   for (int b = 0; b < 3; ++b) {
@@ -276,7 +279,12 @@ extern "C" int moe_ctx_create(const moe_ctx_desc *d, moe_ctx **out) {
       }
       c->presum.push_back(p);
     }
-    cudaError_t se = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
+    int least = 0, greatest = 0;
+    cudaError_t se = cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    if (se == cudaSuccess) se = cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, least);
+    if (se == cudaSuccess) se = cudaStreamCreateWithPriority(&c->hi, cudaStreamNonBlocking, greatest);
+    if (se == cudaSuccess) se = cudaEventCreateWithFlags(&c->ev_hi_in, cudaEventDisableTiming);
+    if (se == cudaSuccess) se = cudaEventCreateWithFlags(&c->ev_hi_out, cudaEventDisableTiming);
     if (se == cudaSuccess) se = cudaEventCreateWithFlags(&c->ev_side_start, cudaEventDisableTiming);
     if (se == cudaSuccess) se = cudaEventCreateWithFlags(&c->ev_presum_done, cudaEventDisableTiming);
     if (se != cudaSuccess) {
@@ -368,6 +376,24 @@ extern "C" int moe_ctx_connect(moe_ctx *ctx, const void *all) {
     ctx->peer_presum[h] = (float *)ptrs[3];
   }
   ctx->connected = true;
+  return MOE_OK;
+}
+
+// moe_step with de-dup: its dispatch kernels run on the context's highest-priority stream
+// (joined to the caller's stream by events on both sides), so the block scheduler serves them
+// ahead of the early k_presum on the side stream.
+void *moe_hi_begin(moe_ctx *ctx, void *stream) {
+  if (!ctx->dedup || !ctx->hi) return stream;
+  if (cudaEventRecord(ctx->ev_hi_in, (cudaStream_t)stream) != cudaSuccess ||
+      cudaStreamWaitEvent(ctx->hi, ctx->ev_hi_in, 0) != cudaSuccess)
+    return stream;
+  return (void *)ctx->hi;
+}
+
+int moe_hi_end(moe_ctx *ctx, void *hi, void *stream) {
+  if (hi == stream) return MOE_OK;
+  MOE_CUDA_TRY(cudaEventRecord(ctx->ev_hi_out, (cudaStream_t)hi));
+  MOE_CUDA_TRY(cudaStreamWaitEvent((cudaStream_t)stream, ctx->ev_hi_out, 0));
   return MOE_OK;
 }
 

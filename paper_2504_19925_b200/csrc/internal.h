@@ -83,7 +83,9 @@ struct moe_ctx {
   bool dedup;
   int nq_max;                  // min(E, S / 3): partial-sum rows per GPU
   std::vector<float *> presum; // [n_local] library-owned
-  cudaStream_t side;           // low-priority stream for the early k_presum (moe_step)
+  cudaStream_t side;           // stream for the early k_presum (moe_step)
+  cudaStream_t hi;             // highest-priority stream for moe_step's dispatch kernels
+  cudaEvent_t ev_hi_in, ev_hi_out;
   cudaEvent_t ev_side_start, ev_presum_done;
   bool presum_ready;           // a k_presum for plan presum_fs is in flight on `side`
   std::vector<int32_t> presum_fs;

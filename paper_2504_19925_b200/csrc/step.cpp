@@ -17,7 +17,10 @@ extern "C" int moe_step(moe_ctx *ctx, const int32_t *topk_ids, const float *gate
   // low-priority side stream, overlapping the dispatch and the host planner
   int st = moe_presum_prelaunch(ctx, plan_cur, stream);
   if (st) return st;
-  st = moe_dispatch(ctx, topk_ids, gates, T, plan_cur, out, stream);  // a0 + a2
+  void *ds = moe_hi_begin(ctx, stream);
+  st = moe_dispatch(ctx, topk_ids, gates, T, plan_cur, out, ds);  // a0 + a2
+  if (st) return moe_step_abort(ctx, st);
+  st = moe_hi_end(ctx, ds, stream);
   if (st) return moe_step_abort(ctx, st);
   st = moe_ctx_wait_counts(ctx);  // C_t on the host
   if (st) return moe_step_abort(ctx, st);

@@ -981,10 +981,9 @@ extern "C" int moe_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_pl
 }
 
 // moe_step's early start of the de-dup partial sums (they need only plan_t and the grads, both
-// ready when the step begins): k_presum on the context's side stream with a persistent grid of
-// 2 CTAs per SM (a quarter of the thread slots, ~64 KB of loads in flight per SM), so the
-// dispatch kernels -- the host planner's critical path -- co-reside instead of queueing
-// behind it.  moe_update then waits on its event instead of launching it.
+// ready when the step begins): k_presum on the context's lowest-priority side stream, one item
+// per CTA, while the dispatch kernels -- the host planner's critical path -- run on the
+// highest-priority stream.  moe_update then waits on its event instead of launching it.
 int moe_presum_prelaunch(moe_ctx *ctx, const moe_plan_t *plan_cur, void *stream) {
   ctx->presum_ready = false;
   if (!ctx->dedup) return MOE_OK;
@@ -999,7 +998,9 @@ int moe_presum_prelaunch(moe_ctx *ctx, const moe_plan_t *plan_cur, void *stream)
   MOE_CUDA_TRY(cudaEventRecord(ctx->ev_side_start, s));
   MOE_CUDA_TRY(cudaStreamWaitEvent(ctx->side, ctx->ev_side_start, 0));
   if (pa.nq_total > 0) {
-    const int64_t grid = std::min<int64_t>((int64_t)pa.nq_total * pa.nchunks, (int64_t)ctx->num_sms * 2);
+    // one item per CTA (non-persistent): the dispatch CTAs, launched on the higher-priority
+    // stream, take every SM slot a retiring presum CTA frees
+    const int64_t grid = std::min<int64_t>((int64_t)pa.nq_total * pa.nchunks, (int64_t)1 << 30);
     const auto pev = timing_begin(ctx, ctx->side);
     k_presum<<<(unsigned)grid, kThreads, 0, ctx->side>>>(pa);
     MOE_CUDA_TRY(cudaGetLastError());
