@@ -45,7 +45,8 @@ def token_dispatch(x_bits, dest_slot, dest_off, xbuf, gates=None) -> None:
         if gates is None:
             xbuf[s, o] = x_bits[t]
         else:
-            row = bf16_to_f32(x_bits[t]) * np.float32(gates[p])    # fp32 multiply, RN
+            with np.errstate(over="ignore", invalid="ignore"):      # IEEE inf/NaN are defined
+                row = bf16_to_f32(x_bits[t]) * np.float32(gates[p])    # fp32 multiply, RN
             xbuf[s, o] = f32_to_bf16_rne(row)
 
 
@@ -63,8 +64,9 @@ def token_combine(xbuf, dest_slot, dest_off, T: int, gates=None) -> np.ndarray:
             if s < 0:
                 continue
             term = bf16_to_f32(xbuf[s, o])
-            if gates is not None:
-                term = np.float32(gates[p]) * term           # fp32 multiply, RN
-            acc = (acc + term).astype(np.float32)            # fp32 add, RN, ascending j
+            with np.errstate(over="ignore", invalid="ignore"):   # IEEE inf/NaN are defined
+                if gates is not None:
+                    term = np.float32(gates[p]) * term           # fp32 multiply, RN
+                acc = (acc + term).astype(np.float32)            # fp32 add, RN, ascending j
         out[t] = f32_to_bf16_rne(acc)
     return out
