@@ -260,6 +260,10 @@ def token_a2a(args, wl, layer, G, rank, Tg, S, peak_hbm, barrier, stream):
     if G > 1:
         dist.all_reduce(rows_t, op=dist.ReduceOp.MAX)
     rows = max(1, int(rows_t.item()))
+    need = S * rows * d * 2
+    if need > (48 << 30):  # drop-free routing can pile a hot expert onto one replica
+        return {"skipped": f"the last iteration's hottest slot has {rows} rows: expert buffers "
+                           f"would need {need / 2**30:.0f} GiB per GPU (use --cf for a capacity)"}
     tx = TokenExchange(layer.ctx, d, rows)
     tx.connect_process_group()
     g = torch.Generator(device="cuda").manual_seed(1234 + rank)

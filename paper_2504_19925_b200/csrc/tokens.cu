@@ -26,6 +26,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -49,7 +50,8 @@ struct TokIpc {
 };
 
 constexpr int kTokU = 4;   // dispatch: 16-byte vectors per lane per row
-constexpr int kCombU = 2;  // combine: per row (two rows in flight -> 4 vectors per lane)
+constexpr int kCombU = 2;  // combine: vectors per lane per row chunk, two rows in flight
+                           // (A/B on one box: 2 beats 4 on GPT-small, ties on Qwen3)
 
 }  // namespace
 
@@ -193,25 +195,10 @@ __global__ void k_tok_wait_done(TokSync *mine, int G, uint32_t epoch, int32_t *e
   if ((int)threadIdx.x < G) wait_flag(&mine->done[threadIdx.x], epoch, err);
 }
 
-__device__ __forceinline__ const uint4 *tok_row(const TokArgs &a, int64_t p, int lane, int c0, float &g,
-                                                bool &ok) {
-  const int s = __ldg(a.dest_slot + p);
-  ok = s >= 0;  // dropped pairs contribute nothing
-  if (!ok) return nullptr;
-  const int off = __ldg(a.dest_off + p);
-  if (off >= a.rows) {
-    if (lane == 0 && c0 == 0) atomicOr(a.err, kErrData);
-    ok = false;
-    return nullptr;
-  }
-  g = a.gate ? __ldg(a.gates + p) : 1.f;
-  const uint32_t h = (uint32_t)s / (uint32_t)a.S;
-  return a.xb[h] + ((int64_t)((uint32_t)s - h * (uint32_t)a.S) * a.rows + off) * a.dv;
-}
-
-__device__ __forceinline__ void tok_accum(const TokArgs &a, float (&acc)[kCombU][8], const uint4 (&y)[kCombU], float g) {
+template <int U>
+__device__ __forceinline__ void tok_accum(const TokArgs &a, float (&acc)[U][8], const uint4 (&y)[U], float g) {
 #pragma unroll
-  for (int u = 0; u < kCombU; ++u) {
+  for (int u = 0; u < U; ++u) {
     const uint32_t wd[4] = {y[u].x, y[u].y, y[u].z, y[u].w};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -226,51 +213,102 @@ __device__ __forceinline__ void tok_accum(const TokArgs &a, float (&acc)[kCombU]
   }
 }
 
-// One warp per (token, chunk) item; the k rows are loaded two at a time (both pairs' loads in
-// flight before either is accumulated), accumulation stays in ascending j (reading C2).
+// A warp per token (grid stride).  Lanes j < k fetch pair j's slot/offset/gate once and turn
+// them into a row pointer (nullptr when dropped); the warp then walks the row in chunks of
+// 32 x kCombU vectors, loading two rows' chunks before accumulating either (shuffled
+// pointers), fp32 adds in ascending j (reading C2).  k > 32 falls back to per-pair loads.
+template <int U>
 __global__ void __launch_bounds__(kThreads) k_tok_combine(TokArgs a) {
   arrive_and_wait(a);
   const int lane = threadIdx.x & 31;
-  const int64_t warps = (int64_t)gridDim.x * (kThreads / 32);
-  const int64_t nch = (a.dv + 32 * kCombU - 1) / (32 * kCombU);
-  const int64_t nitems = a.T * a.n_local * nch;
-  for (int64_t i = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); i < nitems; i += warps) {
-    const uint32_t tok = (uint32_t)i / (uint32_t)nch;  // 32-bit: n_local*T*k < 2^31
-    const int64_t c0 = (int64_t)((uint32_t)i - tok * (uint32_t)nch) * (32 * kCombU);
-    const int v = (int)(tok / (uint32_t)a.T);
-    const int64_t t = (int64_t)(tok - (uint32_t)v * (uint32_t)a.T);
-    const int64_t pbase = (int64_t)v * a.T * a.k + t * a.k;
-    float acc[kCombU][8];
-#pragma unroll
-    for (int u = 0; u < kCombU; ++u)
-#pragma unroll
-      for (int q = 0; q < 8; ++q) acc[u][q] = 0.f;
-    for (int j = 0; j < a.k; j += 2) {
-      float g0 = 1.f, g1 = 1.f;
-      bool ok0, ok1 = false;
-      const uint4 *r0 = tok_row(a, pbase + j, lane, (int)c0, g0, ok0);
-      const uint4 *r1 = (j + 1 < a.k) ? tok_row(a, pbase + j + 1, lane, (int)c0, g1, ok1) : nullptr;
-      uint4 y0[kCombU], y1[kCombU];
-#pragma unroll
-      for (int u = 0; u < kCombU; ++u) {
-        const int64_t c = c0 + u * 32 + lane;
-        if (ok0 && c < a.dv) y0[u] = ldg_nc(r0 + c);  // rows are final before the arrive flags
-        if (ok1 && c < a.dv) y1[u] = ldg_nc(r1 + c);
+  const uint32_t warps = gridDim.x * (kThreads / 32);
+  const uint32_t ntok = (uint32_t)(a.T * a.n_local);  // < 2^31 (moe_ctx_create)
+  for (uint32_t tok = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); tok < ntok; tok += warps) {
+    const uint32_t v = tok / (uint32_t)a.T;
+    const uint32_t t = tok - v * (uint32_t)a.T;
+    const int64_t pbase = ((int64_t)v * a.T + t) * a.k;
+    const uint4 *my_row = nullptr;
+    float my_g = 1.f;
+    if (lane < a.k && lane < 32) {
+      const int s = __ldg(a.dest_slot + pbase + lane);
+      if (s >= 0) {  // dropped pairs contribute nothing
+        const int off = __ldg(a.dest_off + pbase + lane);
+        if (off < a.rows) {
+          const uint32_t h = (uint32_t)s / (uint32_t)a.S;
+          my_row = a.xb[h] + ((int64_t)((uint32_t)s - h * (uint32_t)a.S) * a.rows + off) * a.dv;
+          if (a.gate) my_g = __ldg(a.gates + pbase + lane);
+        } else {
+          atomicOr(a.err, kErrData);
+        }
       }
-      if (ok0) tok_accum(a, acc, y0, g0);
-      if (ok1) tok_accum(a, acc, y1, g1);
     }
-    uint4 *dst = a.dst[v] + t * a.dv;
+    uint4 *dst = a.dst[v] + (int64_t)t * a.dv;
+    for (int64_t c0 = 0; c0 < a.dv; c0 += 32 * U) {
+      float acc[U][8];
 #pragma unroll
-    for (int u = 0; u < kCombU; ++u) {
-      const int64_t c = c0 + u * 32 + lane;
-      if (c < a.dv) {
-        uint4 o;
-        o.x = pack2(acc[u][0], acc[u][1]);
-        o.y = pack2(acc[u][2], acc[u][3]);
-        o.z = pack2(acc[u][4], acc[u][5]);
-        o.w = pack2(acc[u][6], acc[u][7]);
-        dst[c] = o;
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[u][q] = 0.f;
+      for (int j = 0; j < a.k; j += 2) {
+        const uint4 *r0, *r1 = nullptr;
+        float g0, g1 = 1.f;
+        if (j < 32) {
+          r0 = (const uint4 *)__shfl_sync(0xffffffffu, (unsigned long long)my_row, j);
+          g0 = __shfl_sync(0xffffffffu, my_g, j);
+          if (j + 1 < a.k) {
+            r1 = (const uint4 *)__shfl_sync(0xffffffffu, (unsigned long long)my_row, j + 1);
+            g1 = __shfl_sync(0xffffffffu, my_g, j + 1);
+          }
+        } else {  // k > 32: per-pair metadata straight from memory
+          const int64_t p0 = pbase + j;
+          const int s0 = __ldg(a.dest_slot + p0);
+          r0 = nullptr;
+          g0 = 1.f;
+          if (s0 >= 0) {
+            const int off = __ldg(a.dest_off + p0);
+            if (off < a.rows) {
+              const uint32_t h = (uint32_t)s0 / (uint32_t)a.S;
+              r0 = a.xb[h] + ((int64_t)((uint32_t)s0 - h * (uint32_t)a.S) * a.rows + off) * a.dv;
+              if (a.gate) g0 = __ldg(a.gates + p0);
+            } else if (lane == 0 && c0 == 0) {
+              atomicOr(a.err, kErrData);
+            }
+          }
+          if (j + 1 < a.k) {
+            const int s1 = __ldg(a.dest_slot + p0 + 1);
+            if (s1 >= 0) {
+              const int off = __ldg(a.dest_off + p0 + 1);
+              if (off < a.rows) {
+                const uint32_t h = (uint32_t)s1 / (uint32_t)a.S;
+                r1 = a.xb[h] + ((int64_t)((uint32_t)s1 - h * (uint32_t)a.S) * a.rows + off) * a.dv;
+                if (a.gate) g1 = __ldg(a.gates + p0 + 1);
+              } else if (lane == 0 && c0 == 0) {
+                atomicOr(a.err, kErrData);
+              }
+            }
+          }
+        }
+        uint4 y0[U], y1[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t c = c0 + u * 32 + lane;
+          if (r0 && c < a.dv) y0[u] = ldg_nc(r0 + c);  // rows are final before the arrive flags
+          if (r1 && c < a.dv) y1[u] = ldg_nc(r1 + c);
+        }
+        if (r0) tok_accum(a, acc, y0, g0);
+        if (r1) tok_accum(a, acc, y1, g1);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t c = c0 + u * 32 + lane;
+        if (c < a.dv) {
+          uint4 o;
+          o.x = pack2(acc[u][0], acc[u][1]);
+          o.y = pack2(acc[u][2], acc[u][3]);
+          o.z = pack2(acc[u][4], acc[u][5]);
+          o.w = pack2(acc[u][6], acc[u][7]);
+          dst[c] = o;
+        }
       }
     }
   }
@@ -359,7 +397,7 @@ extern "C" int moe_tokx_create(moe_ctx *ctx, int64_t d, int64_t rows, void *cons
     return fail(MOE_ERR_CUDA, "moe_tokx_create: cannot allocate the sync buffer");
   }
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tok_combine, kThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tok_combine<kCombU>, kThreads, 0);
   x->blocks = ctx->num_sms * (per_sm > 0 ? per_sm : 1);
   if (ctx->rank < 0) {
     for (int h = 0; h < ctx->G; ++h) {
@@ -481,7 +519,7 @@ extern "C" int moe_token_combine(moe_tokx *x, void *const *dst, int64_t T, const
   MOE_CUDA_TRY(cudaSetDevice(c->device));
   const bool sync = c->rank >= 0 && c->G > 1;
   a.epoch = sync ? ++x->arrive_epoch : 0;
-  k_tok_combine<<<x->blocks, kThreads, 0, (cudaStream_t)stream>>>(a);
+  k_tok_combine<kCombU><<<x->blocks, kThreads, 0, (cudaStream_t)stream>>>(a);
   MOE_CUDA_TRY(cudaGetLastError());
   return MOE_OK;
 }
