@@ -116,66 +116,90 @@ __device__ __forceinline__ uint4 ldg_nc(const uint4 *p) {
   return v;
 }
 
-// Work item = (token, chunk of 32 x kTokU vectors of its row); a warp walks items with a
-// grid stride and loads item i+stride before storing item i (two rows in flight per warp).
-__device__ __forceinline__ void tok_item(const TokArgs &a, int64_t i, int64_t nch, int &v, int64_t &t,
-                                         int64_t &c0) {
-  // 32-bit division: n_local*T*k < 2^31 (moe_ctx_create) and nch <= d/8
-  const uint32_t tok = (uint32_t)i / (uint32_t)nch;
-  c0 = (int64_t)((uint32_t)i - tok * (uint32_t)nch) * (32 * kTokU);
-  v = (int)(tok / (uint32_t)a.T);
-  t = (int64_t)(tok - (uint32_t)v * (uint32_t)a.T);
-}
-
-__device__ __forceinline__ void tok_load(const TokArgs &a, int64_t i, int64_t nch, int lane, uint4 (&x)[kTokU]) {
-  int v;
-  int64_t t, c0;
-  tok_item(a, i, nch, v, t, c0);
-  const uint4 *src = a.src[v] + t * a.dv;
-#pragma unroll
-  for (int u = 0; u < kTokU; ++u) {
-    const int64_t c = c0 + u * 32 + lane;
-    if (c < a.dv) x[u] = ldg_nc(src + c);
+// Lane j < k of the warp owning token t turns pair j's (slot, offset) into the destination row
+// pointer (nullptr when dropped or out of rows) and fetches its gate.
+__device__ __forceinline__ void tok_dest(const TokArgs &a, int64_t pbase, int lane, int64_t c0, uint4 *&row,
+                                         float &g) {
+  row = nullptr;
+  g = 1.f;
+  if (lane >= a.k) return;
+  const int s = __ldg(a.dest_slot + pbase + lane);
+  if (s < 0) return;  // dropped (reading B1)
+  const int off = __ldg(a.dest_off + pbase + lane);
+  if (off >= a.rows) {
+    if (c0 == 0) atomicOr(a.err, kErrData);
+    return;
   }
+  const uint32_t h = (uint32_t)s / (uint32_t)a.S;
+  row = a.xb[h] + ((int64_t)((uint32_t)s - h * (uint32_t)a.S) * a.rows + off) * a.dv;
+  if (a.gate) g = __ldg(a.gates + pbase + lane);
 }
 
+// A warp per token (grid stride): it reads the token's row ONCE, 32 x kTokU vectors at a time
+// (the next token's first chunk is prefetched before the current stores), and stores each
+// chunk to the k destination rows (pointers shuffled from lanes j < k; k > 32: per-pair loads).
 __global__ void __launch_bounds__(kThreads, 4) k_tok_dispatch(TokArgs a) {
   arrive_and_wait(a);
   const int lane = threadIdx.x & 31;
-  const int64_t warps = (int64_t)gridDim.x * (kThreads / 32);
-  const int64_t nch = (a.dv + 32 * kTokU - 1) / (32 * kTokU);
-  const int64_t nitems = a.T * a.n_local * nch;
-  int64_t i = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  const uint32_t warps = gridDim.x * (kThreads / 32);
+  const uint32_t ntok = (uint32_t)(a.T * a.n_local);  // < 2^31 (moe_ctx_create)
+  uint32_t tok = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
   uint4 x[kTokU];
-  if (i < nitems) tok_load(a, i, nch, lane, x);
-  while (i < nitems) {
-    const int64_t in = i + warps;
-    uint4 xn[kTokU];
-    if (in < nitems) tok_load(a, in, nch, lane, xn);
-    int v;
-    int64_t t, c0;
-    tok_item(a, i, nch, v, t, c0);
-    const int64_t pbase = (int64_t)v * a.T * a.k + t * a.k;
-    for (int j = 0; j < a.k; ++j) {
-      const int s = __ldg(a.dest_slot + pbase + j);
-      if (s < 0) continue;  // dropped (reading B1)
-      const int off = __ldg(a.dest_off + pbase + j);
-      if (off >= a.rows) {
-        if (lane == 0 && c0 == 0) atomicOr(a.err, kErrData);
-        continue;
-      }
-      const uint32_t h = (uint32_t)s / (uint32_t)a.S;
-      uint4 *dst = a.xb[h] + ((int64_t)((uint32_t)s - h * (uint32_t)a.S) * a.rows + off) * a.dv;
-      const float g = a.gate ? __ldg(a.gates + pbase + j) : 1.f;
+  auto load = [&](uint32_t tk, int64_t c0, uint4(&buf)[kTokU]) {
+    const uint32_t v = tk / (uint32_t)a.T;
+    const uint4 *src = a.src[v] + ((int64_t)(tk - v * (uint32_t)a.T)) * a.dv;
 #pragma unroll
-      for (int u = 0; u < kTokU; ++u) {
-        const int64_t c = c0 + u * 32 + lane;
-        if (c < a.dv) dst[c] = a.gate ? scale8(x[u], g) : x[u];
-      }
+    for (int u = 0; u < kTokU; ++u) {
+      const int64_t c = c0 + u * 32 + lane;
+      if (c < a.dv) buf[u] = ldg_nc(src + c);
     }
+  };
+  if (tok < ntok) load(tok, 0, x);
+  for (; tok < ntok; tok += warps) {
+    const uint32_t v = tok / (uint32_t)a.T;
+    const int64_t pbase = ((int64_t)v * a.T + (tok - v * (uint32_t)a.T)) * a.k;
+    uint4 *my_row;
+    float my_g;
+    tok_dest(a, pbase, lane, 0, my_row, my_g);
+    for (int64_t c0 = 0; c0 < a.dv; c0 += 32 * kTokU) {
+      uint4 xn[kTokU];
+      const int64_t cn = c0 + 32 * kTokU;
+      const bool more = cn < a.dv;
+      if (more) load(tok, cn, xn);
+      else if (tok + warps < ntok) load(tok + warps, 0, xn);  // next token's first chunk
+      for (int j = 0; j < a.k; ++j) {
+        uint4 *dst;
+        float g;
+        if (j < 32) {
+          dst = (uint4 *)__shfl_sync(0xffffffffu, (unsigned long long)my_row, j);
+          g = __shfl_sync(0xffffffffu, my_g, j);
+        } else {
+          uint4 *r = nullptr;  // k > 32: lane-independent per-pair metadata
+          float gg = 1.f;
+          const int s = __ldg(a.dest_slot + pbase + j);
+          if (s >= 0) {
+            const int off = __ldg(a.dest_off + pbase + j);
+            if (off < a.rows) {
+              const uint32_t h = (uint32_t)s / (uint32_t)a.S;
+              r = a.xb[h] + ((int64_t)((uint32_t)s - h * (uint32_t)a.S) * a.rows + off) * a.dv;
+              if (a.gate) gg = __ldg(a.gates + pbase + j);
+            } else if (lane == 0 && c0 == 0) {
+              atomicOr(a.err, kErrData);
+            }
+          }
+          dst = r;
+          g = gg;
+        }
+        if (!dst) continue;
 #pragma unroll
-    for (int u = 0; u < kTokU; ++u) x[u] = xn[u];
-    i = in;
+        for (int u = 0; u < kTokU; ++u) {
+          const int64_t c = c0 + u * 32 + lane;
+          if (c < a.dv) dst[c] = a.gate ? scale8(x[u], g) : x[u];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kTokU; ++u) x[u] = xn[u];
+    }
   }
   if (a.rank >= 0 && a.G > 1) {  // barrier-out: the last CTA announces "my rows landed"
     __threadfence_system();
