@@ -242,7 +242,7 @@ __device__ __forceinline__ void tok_accum(const TokArgs &a, float (&acc)[U][8], 
 // 32 x kCombU vectors, loading two rows' chunks before accumulating either (shuffled
 // pointers), fp32 adds in ascending j (reading C2).  k > 32 falls back to per-pair loads.
 template <int U>
-__global__ void __launch_bounds__(kThreads) k_tok_combine(TokArgs a) {
+__global__ void __launch_bounds__(kThreads, 4) k_tok_combine(TokArgs a) {
   arrive_and_wait(a);
   const int lane = threadIdx.x & 31;
   const uint32_t warps = gridDim.x * (kThreads / 32);
