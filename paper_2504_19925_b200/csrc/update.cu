@@ -619,6 +619,9 @@ struct ReplArgs {
   uint16_t *w[MOE_MAX_G];     // local rank v: bf16 slot weights [S][P]
 };
 
+// One CTA row per local slot; only the FIRST slot of an expert with local duplicates works: it
+// reads the remote owners' ranges of that slot once and stores them into every other local
+// slot of the expert (earlier version: one row per duplicate, re-reading the source each time).
 __global__ void __launch_bounds__(kThreads) k_replicate(const __grid_constant__ ReplArgs a) {
   const int v = blockIdx.y / a.S, l = blockIdx.y % a.S;
   const int h = a.o_begin + v;
@@ -629,10 +632,12 @@ __global__ void __launch_bounds__(kThreads) k_replicate(const __grid_constant__ 
     if (a.fs[mid] <= j) lo = mid;
     else hi = mid - 1;
   }
-  const int j0 = max(a.fs[lo], h * a.S);  // GPU h's first slot of that expert
-  if (j == j0) return;
-  const uint16_t *src = a.w[v] + (int64_t)(j0 - h * a.S) * a.P;
-  uint16_t *dst = a.w[v] + (int64_t)l * a.P;
+  const int j0 = max(a.fs[lo], h * a.S);      // GPU h's first slot of that expert
+  const int jb = min(a.fs[lo + 1], (h + 1) * a.S);
+  if (j != j0 || jb - j0 < 2) return;
+  const int ndup = jb - j0 - 1;
+  const uint16_t *src = a.w[v] + (int64_t)l * a.P;
+  uint16_t *dst0 = a.w[v] + (int64_t)(l + 1) * a.P;
   const int64_t nrem = a.P - a.Pg, own = (int64_t)h * a.Pg;  // remote owners' elements
   constexpr int kU = 4;  // 16-byte vectors in flight per thread
   const int64_t stride = (int64_t)gridDim.x * kThreads * kVec;
@@ -643,10 +648,13 @@ __global__ void __launch_bounds__(kThreads) k_replicate(const __grid_constant__ 
       const int64_t r = r0 + u * stride;
       if (r < nrem) buf[u] = ld_stream(src + (r < own ? r : r + a.Pg));
     }
+    for (int d = 0; d < ndup; ++d) {
+      uint16_t *dst = dst0 + (int64_t)d * a.P;
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const int64_t r = r0 + u * stride;
-      if (r < nrem) st_stream(dst + (r < own ? r : r + a.Pg), buf[u]);
+      for (int u = 0; u < kU; ++u) {
+        const int64_t r = r0 + u * stride;
+        if (r < nrem) st_stream(dst + (r < own ? r : r + a.Pg), buf[u]);
+      }
     }
   }
 }
@@ -943,18 +951,18 @@ int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *pl
     ra.P = ctx->P;
     ra.Pg = ctx->Pg;
     for (int e = 0; e <= ctx->E; ++e) ra.fs[e] = plan_next->first_slot[e];
-    int ndup = 0;
+    int nsrc = 0;  // experts with local duplicates (one source each)
     for (int v = 0; v < ctx->n_local; ++v) {
       ra.w[v] = (uint16_t *)ctx->slot_w[v];
       const int h = a.o_begin + v;
       for (int e = 0; e < ctx->E; ++e) {
         const int ja = std::max(ra.fs[e], h * ctx->S), jb = std::min(ra.fs[e + 1], (h + 1) * ctx->S);
-        if (jb - ja > 1) ndup += jb - ja - 1;
+        if (jb - ja > 1) ++nsrc;
       }
     }
-    if (ndup > 0) {
+    if (nsrc > 0) {
       const int gx = std::max(1, std::min<int>((int)((ctx->P - ctx->Pg) / (kThreads * kVec)) + 1,
-                                               8 * ctx->num_sms / ndup + 1));
+                                               8 * ctx->num_sms / nsrc + 1));
       const auto rev = timing_begin(ctx, s);
       k_replicate<<<dim3(gx, ctx->n_local * ctx->S), kThreads, 0, s>>>(ra);
       MOE_CUDA_TRY(cudaGetLastError());
