@@ -155,6 +155,30 @@ def run_oracle_sample(wl, G: int, iters: int, frac_den: int = 256, seed_shift: i
     sample), extrapolated x frac_den (every stage after dispatch is elementwise per expert).
     Returns (ms per full iteration, description, per-iteration seconds)."""
     os.environ.setdefault("OMP_NUM_THREADS", "1")
+    # SURVEY d.5: one host core (pinned for the timing, restored after)
+    prev_aff = os.sched_getaffinity(0) if hasattr(os, "sched_getaffinity") else None
+    if prev_aff:
+        os.sched_setaffinity(0, {min(prev_aff)})
+    try:
+        return _run_oracle_sample(wl, G, iters, frac_den, seed_shift)
+    finally:
+        if prev_aff:
+            os.sched_setaffinity(0, prev_aff)
+
+
+def host_info() -> dict:
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "host_cores": os.cpu_count(), "pinned_cores": 1}
+
+
+def _run_oracle_sample(wl, G: int, iters: int, frac_den: int, seed_shift: int):
     from oracle import dispatch as od
     from oracle import plan as op
     from oracle import step as ostep
@@ -199,7 +223,7 @@ def reference_arm(args, wl):
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "config": _config(wl, G),
         "cpu_baseline": {"value": round(val, 3), "unit": "ms/iter", "cores": 1, "kind": "oracle",
-                         "sample": desc},
+                         "sample": desc, "host": host_info()},
         "e2e": {"value": round(val, 3), "unit": "ms/iter", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "wall_s": round(time.perf_counter() - t0, 1),
@@ -387,10 +411,13 @@ def gpu_arm(args, wl):
     layer.ctx.get_timing()                          # clear
     layer.ctx.set_timing(True)                      # library events around its own launches
     barrier()
+    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
     start.record(stream)
     h0 = time.perf_counter()
+    step_ev[0].record(stream)
     for i in range(K):
         step(args.warmup + i, record=True)
+        step_ev[i + 1].record(stream)
     h1 = time.perf_counter()
     end.record(stream)
     barrier()
@@ -411,6 +438,15 @@ def gpu_arm(args, wl):
     if G > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms, upd_avg, disp_avg, pre_avg, rep_avg, updk_avg = (float(x) for x in t.tolist())
+    # per-iteration step times, max over ranks (SURVEY d.4: median, p10, p90)
+    per_step = torch.tensor([step_ev[i].elapsed_time(step_ev[i + 1]) for i in range(K)], device="cuda")
+    if G > 1:
+        dist.all_reduce(per_step, op=dist.ReduceOp.MAX)
+    ps = sorted(float(x) for x in per_step.tolist())
+    def _q(f):
+        return round(ps[min(len(ps) - 1, int(f * (len(ps) - 1) + 0.5))], 4)
+    step_dist = {"p10": _q(0.1), "median": _q(0.5), "p90": _q(0.9), "min": round(ps[0], 4),
+                 "max": round(ps[-1], 4), "note": "per-iteration CUDA-event times, max over ranks"}
     host_ms = 1e3 * (h1 - h0) / K
     ms_iter = total_ms / K
 
@@ -487,6 +523,9 @@ def gpu_arm(args, wl):
                 "traffic": args.traffic if (G == 1 and not args.dedup) else None,
                 "algorithmic_bytes_per_launch": int(mean["update_hbm"]), "peak_source": peak_src,
                 "avg_launch_ms": round(updk_avg, 4)}
+    nominal = {"hbm": 8000.0, "nvlink": 900.0}.get(roof["bound"])
+    if nominal:  # north_star's 8 TB/s HBM (SURVEY d.2) / NVLink 5's 900 GB/s, for context
+        roof["nominal"] = {"peak": nominal, "frac": round(roof["achieved"] / nominal, 4)}
     disp_hbm = 28 * (wl.T // G) * wl.k
     # whole step: every HBM byte of dispatch + update stage at the HBM peak, or the NVLink bytes
     t_roof_step = max((mean["stage_hbm"] + disp_hbm) / (peak_hbm * 1e9), t_nvl, t_pcie)
@@ -498,7 +537,8 @@ def gpu_arm(args, wl):
     cpu = None
     if rank == 0 and G == 1 and not args.no_cpu_baseline:
         ms, desc, _ = run_oracle_sample(wl, G, args.cpu_iters, frac_den=args.cpu_frac)
-        cpu = {"value": round(ms, 1), "unit": "ms/iter", "cores": 1, "kind": "oracle", "sample": desc}
+        cpu = {"value": round(ms, 1), "unit": "ms/iter", "cores": 1, "kind": "oracle", "sample": desc,
+               "host": host_info()}
 
     if rank == 0:
         line = {
@@ -510,6 +550,7 @@ def gpu_arm(args, wl):
                            policy=args.policy,
                            replan_interval=args.interval, capacity_factor=args.cf or None),
             "roofline": roof,
+            "step_ms_dist": step_dist,
             "step_roofline": {"t_roof_ms": round(t_roof_step * 1e3, 4),
                               "frac": round(t_roof_step * 1e3 / ms_iter, 4),
                               "basis": "max(HBM bytes of dispatch+update / peak HBM, NVLink bytes/dir / 770 GB/s"
