@@ -61,7 +61,10 @@ __global__ void __launch_bounds__(kThreads) k_hist(const __grid_constant__ HistA
     int e = in ? __ldg(ids + p) : -1;
     bool valid = in && (unsigned)e < (unsigned)a.E;
     if (in && !valid) atomicOr(a.err, kErrData);
-    if (valid && a.k > 1) {  // the k experts of a token must be distinct
+    // the k experts of a token must be distinct.  k | 32: a token's pairs are k aligned lanes
+    // of this warp (tiles and rounds start at multiples of 32), so the expert-match mask
+    // below answers it; otherwise re-read the token's earlier ids.
+    if (valid && a.k > 1 && (32 % a.k) != 0) {
       const int j = (int)(p % a.k);
       for (int jj = 0; jj < j; ++jj)
         if (__ldg(ids + (p - j + jj)) == e) atomicOr(a.err, kErrData);
@@ -69,6 +72,10 @@ __global__ void __launch_bounds__(kThreads) k_hist(const __grid_constant__ HistA
     const unsigned act = __ballot_sync(0xffffffffu, valid);
     if (valid) {
       const unsigned peers = __match_any_sync(act, e);
+      if (a.k > 1 && (32 % a.k) == 0) {
+        const unsigned tok = (a.k == 32 ? 0xffffffffu : ((1u << a.k) - 1u)) << (lane / a.k * a.k);
+        if (__popc(peers & tok) > 1) atomicOr(a.err, kErrData);
+      }
       if (lane == __ffs(peers) - 1) atomicAdd(&hist[e], __popc(peers));
     }
   }
@@ -225,7 +232,9 @@ __global__ void __launch_bounds__(kThreads) k_scan(const __grid_constant__ ScanA
     block_exclusive_scan(dropped, wsum, &dtot);
     if (tid == 0) a.drops[e] = dtot;
   }
-  if (tid == 0) a.einfo[v * a.E + e] = ExpertInfo{base, carry, q, m};
+  if (tid == 0)
+    a.einfo[v * a.E + e] = ExpertInfo{base, carry, q, m, 0xffffffffu / (uint32_t)(q + 1),
+                                      q > 0 ? 0xffffffffu / (uint32_t)q : 0u};
   __syncthreads();  // wsum is reused by the tile scan below
 
   // exclusive scan of this rank's tile counts of expert e, in place
@@ -389,7 +398,8 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ Sc
     const int32_t R = info.base + lr;  // global rank within expert e
     const int32_t q = info.q, m = info.m;
     const int32_t big = m * (q + 1);
-    const int32_t rho = R < big ? R / (q + 1) : m + (R - big) / q;
+    const int32_t rho = R < big ? (int32_t)udiv_fast((uint32_t)R, (uint32_t)(q + 1), info.rq1)
+                                : m + (int32_t)udiv_fast((uint32_t)(R - big), (uint32_t)q, info.rq);
     const int32_t start = rho * q + min(rho, m);
     const int32_t off = R - start;
     if (off >= capv) {  // row f2: beyond the replica's capacity -> dropped, not sent

@@ -38,7 +38,21 @@ struct ExpertInfo {
   int32_t base;     // global rank of this rank's first pair of the expert
   int32_t kcnt;     // this rank's kept pairs of the expert (all of them without capacity)
   int32_t q, m;     // C_e / r_e, C_e % r_e
+  uint32_t rq1, rq; // floor((2^32 - 1) / (q + 1)), floor((2^32 - 1) / q) (0 if q == 0): the
+                    // scatter's divisions as multiply-high + one correction (udiv_fast)
 };
+
+// n / d for 0 <= n < 2^31, 1 <= d < 2^31, with rd = floor((2^32 - 1) / d): the estimate
+// __umulhi(n, rd) is exact or one short, fixed by one compare.
+__host__ __device__ __forceinline__ uint32_t udiv_fast(uint32_t n, uint32_t d, uint32_t rd) {
+#ifdef __CUDA_ARCH__
+  uint32_t qt = __umulhi(n, rd);
+#else
+  uint32_t qt = (uint32_t)(((uint64_t)n * rd) >> 32);
+#endif
+  if (n - qt * d >= d) ++qt;
+  return qt;
+}
 
 struct IpcRecord {
   cudaIpcMemHandle_t h[4];  // slot_g, slot_w, sync, presum (zeroed when absent)

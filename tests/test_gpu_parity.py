@@ -257,3 +257,26 @@ def test_host_state_pointer_checks():
         assert L.lib().moe_ctx_create(C.byref(desc), C.byref(h)) == 1
         assert b"host" in L.lib().moe_last_error()
         lay.close()
+
+
+@pytest.mark.parametrize("k", [2, 3, 4, 8])
+def test_repeated_expert_within_token_detected(k):
+    """k | 32 uses the in-warp expert-match mask, other k re-read the token's ids: both must
+    flag a repeat anywhere in a token, and only then (tokens at every lane offset)."""
+    from paper_2504_19925_b200 import DecoupledExpertLayer, MoeError
+    E, T = 16, 1000
+    layer = DecoupledExpertLayer(E, 1, 16, k, 64, T, rank=0, device=0)
+    rng = np.random.default_rng(k)
+    base = np.stack([rng.permutation(E)[:k] for _ in range(T)]).astype(np.int32)
+    gates = torch.ones((T, k), dtype=torch.float32, device="cuda")
+    layer.dispatch(torch.from_numpy(base).cuda(), gates, T)
+    layer.ctx.check()                                  # distinct: clean
+    for t in (0, 1, 7, 31, 517, T - 1):
+        for (j0, j1) in ((0, k - 1), (k - 2, k - 1)):
+            ids = base.copy()
+            ids[t, j1] = ids[t, j0]
+            layer.dispatch(torch.from_numpy(ids).cuda(), gates, T)
+            with pytest.raises(MoeError) as ei:
+                layer.ctx.check()
+            assert ei.value.status == 3, (t, j0, j1)
+    layer.close()
