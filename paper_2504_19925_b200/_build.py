@@ -24,7 +24,7 @@ OBJ = os.path.join(HERE, "build")
 
 CU = ["ctx.cu", "dispatch.cu", "update.cu", "synth.cu", "tokens.cu"]
 CPP = ["plan.cpp", "step.cpp"]
-HEADERS = [os.path.join(CSRC, h) for h in ("common.h", "internal.h")] + \
+HEADERS = [os.path.join(CSRC, h) for h in ("common.h", "internal.h", "fastdiv.h")] + \
     [os.path.join(INC, h) for h in ("moe_dc.h", "moe_synth.h", "moe_tokens.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -292,6 +292,7 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ Sc
   __shared__ ExpertInfo s_info[MOE_MAX_E];
   __shared__ int32_t s_blk[MOE_MAX_E];
   __shared__ int32_t s_loc[MOE_MAX_E];  // where expert e's kept pairs start in this rank's send order
+  __shared__ int32_t s_fs[MOE_MAX_E + 1];  // plan_t (lane-divergent reads: not from the param bank)
   extern __shared__ int32_t s_tile[];  // [tile] ids, then [tile] gates (bit patterns)
   const int v = blockIdx.x / a.nb;
   const int b = blockIdx.x % a.nb;
@@ -312,6 +313,7 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ Sc
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) wcnt[w][e] = 0;
   }
+  for (int e = tid; e <= a.E; e += kThreads) s_fs[e] = a.fs[e];
   __syncthreads();
   if (warp == 0) {  // s_loc = exclusive prefix over experts of this rank's kept counts
     constexpr int kPer = MOE_MAX_E / 32;
@@ -342,9 +344,10 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ Sc
 
   // Warp w owns the consecutive pairs [w*R*32, (w+1)*R*32) of the tile (R = tile/256 rounds of
   // 32): pair order == (warp, round, lane) order, so the ranks below are stable.
-  // Pass 1 counts each warp's pairs per expert; an exclusive prefix over warps turns the
-  // counts into starting ranks; pass 2 re-walks the segment, ranking each pair as
-  // start + (lower lanes of the round with the same expert) and advancing the start.
+  // Pass 1 ranks each pair within its warp's pairs of the same expert -- the warp's running
+  // count of e before this round + the lower lanes of the round with e (__match_any_sync) --
+  // and packs (rank << 8 | e) into the staged id; an exclusive prefix over warps then turns
+  // the per-warp totals into starting ranks, and pass 2 needs no further matching.
   const int rounds = a.tile / kThreads;
   const int64_t seg = (int64_t)b * a.tile + (int64_t)warp * rounds * 32;
   const unsigned lt = (1u << lane) - 1u;
@@ -355,10 +358,15 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ Sc
     const int e = in ? s_tile[p - tbase] : -1;
     const bool valid = in && (unsigned)e < (unsigned)a.E;
     const unsigned act = __ballot_sync(0xffffffffu, valid);
+    unsigned peers = 0;
+    int32_t wr = 0;
     if (valid) {
-      const unsigned peers = __match_any_sync(act, e);
-      if (lane == __ffs(peers) - 1) wcnt[warp][e] += __popc(peers);
+      peers = __match_any_sync(act, e);
+      wr = wcnt[warp][e] + __popc(peers & lt);
     }
+    __syncwarp();
+    if (valid && lane == __ffs(peers) - 1) wcnt[warp][e] += __popc(peers);
+    if (in) s_tile[p - tbase] = valid ? (wr << 8) | e : -1;  // E <= 256, wr < tile
     __syncwarp();
   }
   __syncthreads();
@@ -374,25 +382,15 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ Sc
   __syncthreads();
   for (int r = 0; r < rounds; ++r) {  // pass 2
     const int64_t p = seg + r * 32 + lane;
-    const bool in = p < a.npairs;
-    const int e = in ? s_tile[p - tbase] : -1;
-    const bool valid = in && (unsigned)e < (unsigned)a.E;
-    const unsigned act = __ballot_sync(0xffffffffu, valid);
-    unsigned peers = 0;
-    int32_t wr = 0;
-    if (valid) {
-      peers = __match_any_sync(act, e);
-      wr = wcnt[warp][e] + __popc(peers & lt);
-    }
-    __syncwarp();
-    if (valid && lane == __ffs(peers) - 1) wcnt[warp][e] += __popc(peers);
-    __syncwarp();
-    if (!in) continue;
-    if (!valid) {  // invalid id: flagged by k_hist; keep memory safe
+    if (p >= a.npairs) break;
+    const int32_t x = s_tile[p - tbase];
+    if (x < 0) {  // invalid id: flagged by k_hist; keep memory safe
       a.dest_slot[off_v + p] = -1;
       a.dest_off[off_v + p] = -1;
       continue;
     }
+    const int e = x & 0xff;
+    const int32_t wr = wcnt[warp][e] + (x >> 8);
     const ExpertInfo info = s_info[e];
     const int32_t lr = s_blk[e] + wr;  // rank within this rank's pairs of e
     const int32_t R = info.base + lr;  // global rank within expert e
@@ -407,13 +405,13 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ Sc
       a.dest_off[off_v + p] = -1;
       continue;
     }
-    const int32_t slot = a.fs[e] + rho;
+    const int32_t slot = s_fs[e] + rho;
     a.dest_slot[off_v + p] = slot;
     a.dest_off[off_v + p] = off;
     // slot-major position among this rank's kept pairs: experts before e, kept pairs of this
     // rank in e's earlier replicas, then this rank's pairs in replica rho before this one
     // (all kept: a replica keeps a prefix of its offsets)
-    const int64_t pos = off_v + s_loc[e] + kept_pre[slot] + (R - max(info.base, start));
+    const int64_t pos = off_v + s_loc[e] + __ldg(kept_pre + slot) + (R - max(info.base, start));
     a.send_pair[pos] = (int32_t)p;
     a.send_gate[pos] = __int_as_float(s_tile[a.tile + (p - tbase)]);
   }
@@ -551,8 +549,15 @@ extern "C" int moe_dispatch(moe_ctx *ctx, const int32_t *topk_ids, const float *
   ca.cap = out->capacity;
   ca.kept_pre = ctx->kept_pre;
   for (int e = 0; e <= ctx->E; ++e) ca.fs[e] = plan->first_slot[e];
-  if (npairs > 0)
+  if (npairs > 0) {
+    static bool smem_opt_in = false;  // static smem (~17 KB) + 2 x tile ints can exceed 48 KB
+    if (!smem_opt_in) {
+      MOE_CUDA_TRY(cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)(2 * kMaxTilePairs * sizeof(int32_t))));
+      smem_opt_in = true;
+    }
     MOE_CUDA_TRY(launch_pdl(k_scatter, dim3(nb * ctx->n_local), s, ca, (size_t)2 * tile * sizeof(int32_t)));
+  }
   timing_end(ctx->ev_disp, tev, s);
   return MOE_OK;
 }

@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "common.h"
+#include "fastdiv.h"
 
 namespace moe {
 
@@ -42,17 +43,7 @@ struct ExpertInfo {
                     // scatter's divisions as multiply-high + one correction (udiv_fast)
 };
 
-// n / d for 0 <= n < 2^31, 1 <= d < 2^31, with rd = floor((2^32 - 1) / d): the estimate
-// __umulhi(n, rd) is exact or one short, fixed by one compare.
-__host__ __device__ __forceinline__ uint32_t udiv_fast(uint32_t n, uint32_t d, uint32_t rd) {
-#ifdef __CUDA_ARCH__
-  uint32_t qt = __umulhi(n, rd);
-#else
-  uint32_t qt = (uint32_t)(((uint64_t)n * rd) >> 32);
-#endif
-  if (n - qt * d >= d) ++qt;
-  return qt;
-}
+
 
 struct IpcRecord {
   cudaIpcMemHandle_t h[4];  // slot_g, slot_w, sync, presum (zeroed when absent)
