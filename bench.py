@@ -258,7 +258,26 @@ def measure_pcie(device: int, nbytes: int = 1 << 30) -> dict:
             b.synchronize()
             best = min(best, a.elapsed_time(b))
         out[name] = nbytes / (best * 1e-3) / 1e9
-    del h, d
+    # both directions at once on two streams (what the staging pipeline does)
+    h2, d2 = torch.empty_like(h), torch.empty_like(d)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    best = 1e9
+    for _ in range(5):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        s1.wait_event(a)
+        s2.wait_event(a)
+        with torch.cuda.stream(s1):
+            d.copy_(h, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h2.copy_(d2, non_blocking=True)
+        torch.cuda.current_stream().wait_stream(s1)
+        torch.cuda.current_stream().wait_stream(s2)
+        b.record()
+        b.synchronize()
+        best = min(best, a.elapsed_time(b))
+    out["bidir_gbs_per_dir"] = nbytes / (best * 1e-3) / 1e9
+    del h, d, h2, d2
     return out
 
 
@@ -497,16 +516,19 @@ def gpu_arm(args, wl):
     t_nvl = mean["nvl"] / (GUIDE_NVLINK_GBS * 1e9) if G > 1 else 0.0
     kname = "k_update_tma (fused reduce+Adam+place" + (", de-dup)" if args.dedup else ")")
     pcie = measure_pcie(local) if args.host_state else None
-    t_pcie = mean["pcie_per_dir"] / (min(pcie["h2d_gbs"], pcie["d2h_gbs"]) * 1e9) if pcie else 0.0
+    # the staging pipeline runs H2D and D2H at once: its peak is the bidirectional copy rate
+    pk_pcie = min(pcie["h2d_gbs"], pcie["d2h_gbs"], pcie["bidir_gbs_per_dir"]) if pcie else 0.0
+    t_pcie = mean["pcie_per_dir"] / (pk_pcie * 1e9) if pcie else 0.0
     if t_pcie > max(t_nvl, t_hbm_k):   # row f4: the state streams over PCIe
         achieved = mean["pcie_per_dir"] / (updk_avg * 1e-3) / 1e9
-        pk = min(pcie["h2d_gbs"], pcie["d2h_gbs"])
+        pk = pk_pcie
         roof = {"kernel": kname + " + copy-engine staging of the host-resident state", "bound": "pcie",
                 "achieved": round(achieved, 1), "peak": round(pk, 1), "unit": "GB/s",
                 "frac": round(achieved / pk, 4), "traffic": None,
                 "algorithmic_bytes_per_launch": int(mean["pcie_per_dir"]),
                 "peak_source": "measured in this run, all ranks at once: pinned<->device torch copies "
-                               f"of 1 GiB, H2D {pcie['h2d_gbs']:.1f} / D2H {pcie['d2h_gbs']:.1f} GB/s (min)",
+                               f"of 1 GiB, H2D {pcie['h2d_gbs']:.1f} / D2H {pcie['d2h_gbs']:.1f} / both "
+                               f"directions at once {pcie['bidir_gbs_per_dir']:.1f} GB/s per direction (min)",
                 "avg_launch_ms": round(updk_avg, 4)}
     elif t_nvl > t_hbm_k:
         achieved = mean["nvl"] / (updk_avg * 1e-3) / 1e9
