@@ -259,7 +259,8 @@ def measure_pcie(device: int, nbytes: int = 1 << 30) -> dict:
             best = min(best, a.elapsed_time(b))
         out[name] = nbytes / (best * 1e-3) / 1e9
     # both directions at once on two streams (what the staging pipeline does)
-    h2, d2 = torch.empty_like(h), torch.empty_like(d)
+    h2 = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d2 = torch.empty_like(d)
     s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
     best = 1e9
     for _ in range(5):

@@ -241,9 +241,9 @@ extern "C" int moe_ctx_create(const moe_ctx_desc *d, moe_ctx **out) {
     const char *k = getenv("MOE_UPDATE_KERNEL");
     c->update_kernel = (k && std::string(k) == "ldg") ? 0 : 1;
   }
-  if (c->host_state) {  // row f4: three staging windows of ~32 MB of state each, two copy streams
+  if (c->host_state) {  // row f4: three staging windows of ~64 MB of state each, two copy streams
     const int64_t pg_pad = (c->Pg + kChunk - 1) / kChunk * kChunk;
-    int64_t w = ((int64_t)32 << 20) / (12 * (int64_t)c->E * n_local) / kChunk * kChunk;
+    int64_t w = ((int64_t)64 << 20) / (12 * (int64_t)c->E * n_local) / kChunk * kChunk;
     c->hs_w = std::min<int64_t>(pg_pad, std::max<int64_t>(kChunk, w));
     cudaError_t he = cudaSuccess;
     auto hchk = [&](cudaError_t x) {
