@@ -21,7 +21,8 @@
 
 using namespace moe;
 
-int moe_update_init();  // update.cu
+int moe_update_init();    // update.cu
+int moe_dispatch_init();  // dispatch.cu
 
 int moe_validate_plan(const moe_ctx *ctx, const moe_plan_t *p, const char *what) {
   if (!p || !p->first_slot) return fail(MOE_ERR_INVALID, "%s: NULL plan", what);
@@ -77,6 +78,7 @@ void free_ctx(moe_ctx *c) {
   cudaFree(c->err);
   cudaFree(c->item_ctr);
   cudaFree(c->scan_done);
+  cudaFree(c->ktrace);
   for (float *p : c->presum) cudaFree(p);
   if (c->side) cudaStreamDestroy(c->side);
   if (c->hi) cudaStreamDestroy(c->hi);
@@ -231,6 +233,10 @@ extern "C" int moe_ctx_create(const moe_ctx_desc *d, moe_ctx **out) {
   if (e != cudaSuccess) {
     free_ctx(c);
     return fail(MOE_ERR_CUDA, "moe_ctx_create: %s", cudaGetErrorString(e));
+  }
+  if (moe_dispatch_init() != MOE_OK) {
+    free_ctx(c);
+    return fail(MOE_ERR_CUDA, "moe_ctx_create: dispatch kernel setup failed");
   }
   c->upd_blocks_per_sm = moe_update_init();
   if (c->upd_blocks_per_sm < 0) {

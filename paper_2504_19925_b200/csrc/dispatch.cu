@@ -424,6 +424,14 @@ using namespace moe;
 
 int moe_validate_plan(const moe_ctx *ctx, const moe_plan_t *p, const char *what);  // ctx.cu
 
+// Per-device kernel attributes of the dispatch (called by moe_ctx_create on ctx->device):
+// k_scatter's static smem (~17 KB) + 2 x tile ints of staged ids/gates can exceed 48 KB.
+int moe_dispatch_init() {
+  MOE_CUDA_TRY(cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)(2 * kMaxTilePairs * sizeof(int32_t))));
+  return MOE_OK;
+}
+
 namespace {
 // Launch with programmatic stream serialization (PDL): overlaps this kernel's launch with the
 // tail of the previous kernel in the stream; the kernel calls pdl_wait() before reading it.
@@ -549,15 +557,8 @@ extern "C" int moe_dispatch(moe_ctx *ctx, const int32_t *topk_ids, const float *
   ca.cap = out->capacity;
   ca.kept_pre = ctx->kept_pre;
   for (int e = 0; e <= ctx->E; ++e) ca.fs[e] = plan->first_slot[e];
-  if (npairs > 0) {
-    static bool smem_opt_in = false;  // static smem (~17 KB) + 2 x tile ints can exceed 48 KB
-    if (!smem_opt_in) {
-      MOE_CUDA_TRY(cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)(2 * kMaxTilePairs * sizeof(int32_t))));
-      smem_opt_in = true;
-    }
+  if (npairs > 0)
     MOE_CUDA_TRY(launch_pdl(k_scatter, dim3(nb * ctx->n_local), s, ca, (size_t)2 * tile * sizeof(int32_t)));
-  }
   timing_end(ctx->ev_disp, tev, s);
   return MOE_OK;
 }

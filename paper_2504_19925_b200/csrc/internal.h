@@ -110,6 +110,7 @@ struct moe_ctx {
   volatile uint32_t *host_flag;  // pinned host word: k_scan writes the dispatch epoch once C_e landed
   uint32_t *host_flag_dev;       // its device (UVA) alias
   bool counts_pending;
+  unsigned long long *ktrace;    // MOE_KTRACE development trace scratch (lazily allocated)
 
   std::map<std::string, void *> opened;  // IPC handle bytes -> mapped base (dedup)
 

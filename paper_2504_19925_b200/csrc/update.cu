@@ -848,9 +848,9 @@ int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *pl
     k_barrier<<<1, 32, 0, s>>>(ba);
     MOE_CUDA_TRY(cudaGetLastError());
   }
-  static const bool ktrace_on = getenv("MOE_KTRACE") != nullptr;
-  static unsigned long long *ktrace_buf = nullptr;
-  if (ktrace_on && tma && !ktrace_buf) MOE_CUDA_TRY(cudaMalloc(&ktrace_buf, 8 * sizeof(unsigned long long)));
+  static const bool ktrace_on = getenv("MOE_KTRACE") != nullptr;  // development trace only
+  if (ktrace_on && tma && !ctx->ktrace) MOE_CUDA_TRY(cudaMalloc(&ctx->ktrace, 8 * sizeof(unsigned long long)));
+  unsigned long long *ktrace_buf = ctx->ktrace;
   // one launch of the fused kernel over a's chunk window
   auto run_kernel = [&](UpdArgs &ka) -> int {
     ka.ktrace = nullptr;
