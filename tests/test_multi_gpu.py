@@ -45,3 +45,14 @@ def test_real_multi_gpu_parity(G, config, extra):
     r = _torchrun(G, "--config", config, *extra)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "OK" in r.stdout
+
+
+def test_missing_peer_times_out_instead_of_hanging():
+    """Failure detection: a rank that skips an iteration -> MOE_ERR_TIMEOUT on its peer (~30 s)."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(ROOT, "tests", "mp_failure.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert r.returncode == 0 and "mp_failure: OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
