@@ -403,6 +403,12 @@ int moe_hi_end(moe_ctx *ctx, void *hi, void *stream) {
   return MOE_OK;
 }
 
+void moe_host_time(moe_ctx *ctx, int which, double ms) {
+  if (!ctx->timing) return;
+  ctx->host_ms[which] += ms;
+  ++ctx->host_n[which];
+}
+
 extern "C" int moe_ctx_wait_counts(moe_ctx *ctx) {
   if (!ctx) return fail(MOE_ERR_INVALID, "moe_ctx_wait_counts: NULL ctx");
   if (!ctx->counts_pending) return MOE_OK;
@@ -433,9 +439,11 @@ extern "C" int moe_ctx_get_timing_ex(moe_ctx *ctx, double *ms_out, int64_t *n_ou
   MOE_CUDA_TRY(cudaSetDevice(ctx->device));
   double sums[MOE_TIMING_STAGES] = {0.0};
   int64_t counts[MOE_TIMING_STAGES] = {0};
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> *lists[MOE_TIMING_STAGES] = {
+  constexpr int kDeviceStages = 5;  // MOE_T_DISPATCH .. MOE_T_STAGE: CUDA-event pairs
+  static_assert(MOE_T_STAGE == kDeviceStages - 1, "device timing stages");
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> *lists[kDeviceStages] = {
       &ctx->ev_disp, &ctx->ev_upd, &ctx->ev_presum, &ctx->ev_repl, &ctx->ev_stage};
-  for (int k = 0; k < MOE_TIMING_STAGES; ++k) {
+  for (int k = 0; k < kDeviceStages; ++k) {
     for (auto &p : *lists[k]) {
       float ms = 0.f;
       MOE_CUDA_TRY(cudaEventSynchronize(p.second));
@@ -446,6 +454,12 @@ extern "C" int moe_ctx_get_timing_ex(moe_ctx *ctx, double *ms_out, int64_t *n_ou
     }
     lists[k]->clear();
   }
+  sums[MOE_T_HOST_WAIT] = ctx->host_ms[0];
+  counts[MOE_T_HOST_WAIT] = ctx->host_n[0];
+  sums[MOE_T_HOST_PLAN] = ctx->host_ms[1];
+  counts[MOE_T_HOST_PLAN] = ctx->host_n[1];
+  ctx->host_ms[0] = ctx->host_ms[1] = 0.0;
+  ctx->host_n[0] = ctx->host_n[1] = 0;
   // without de-dup the stage is the update kernel itself
   if (counts[MOE_T_STAGE] == 0) {
     sums[MOE_T_STAGE] = sums[MOE_T_UPDATE];

@@ -5,6 +5,8 @@
 // "may execute earlier, even right after step 1", PAPER.md:709 fn), then reduce + Adam +
 // place (a3-a5).  The host planner runs while the device still executes the scatter kernel,
 // and the update is enqueued as soon as the plan exists.
+#include <chrono>
+
 #include "common.h"
 
 extern "C" int moe_step(moe_ctx *ctx, const int32_t *topk_ids, const float *gates, int64_t T,
@@ -22,8 +24,11 @@ extern "C" int moe_step(moe_ctx *ctx, const int32_t *topk_ids, const float *gate
   if (st) return moe_step_abort(ctx, st);
   st = moe_hi_end(ctx, ds, stream);
   if (st) return moe_step_abort(ctx, st);
+  using clk = std::chrono::steady_clock;
+  const auto t0 = clk::now();
   st = moe_ctx_wait_counts(ctx);  // C_t on the host
   if (st) return moe_step_abort(ctx, st);
+  const auto t1 = clk::now();
   if (policy == MOE_PLAN_KEEP) {  // interval policy between re-plans: plan_{t+1} = plan_t
     if (!plan_next->replicas || !plan_next->first_slot || !plan_next->slot_expert || !plan_cur->replicas ||
         !plan_cur->slot_expert)
@@ -40,5 +45,7 @@ extern "C" int moe_step(moe_ctx *ctx, const int32_t *topk_ids, const float *gate
                      nullptr);  // a1 -> plan_{t+1}
     if (st) return moe_step_abort(ctx, st);
   }
+  moe_host_time(ctx, 0, std::chrono::duration<double, std::milli>(t1 - t0).count());
+  moe_host_time(ctx, 1, std::chrono::duration<double, std::milli>(clk::now() - t1).count());
   return moe_update(ctx, plan_cur, plan_next, adam, stream);  // a3 + a4 + a5
 }
