@@ -392,7 +392,7 @@ def gpu_arm(args, wl):
     layer = DecoupledExpertLayer(wl.E, G, S, wl.k, wl.P, Tg, rank=rank if G > 1 else 0,
                                  device=local, seed=seed, dedup=args.dedup, policy=pol,
                                  capacity=cap, replan_interval=args.interval,
-                                 host_state=args.host_state)
+                                 host_state=args.host_state, lazy_replicate=args.lazy)
     if G > 1:
         layer.connect()
     n_tr = min(args.warmup + args.steps, args.trace_iters)
@@ -439,6 +439,7 @@ def gpu_arm(args, wl):
         step(args.warmup + i, record=True)
         step_ev[i + 1].record(stream)
     h1 = time.perf_counter()
+    layer.sync_weights(stream)      # the last step's (possibly deferred) replication is timed too
     end.record(stream)
     barrier()
     clocks = clk.stop()
@@ -491,6 +492,7 @@ def gpu_arm(args, wl):
             layer.slot_g[0].copy_(grads_h, non_blocking=True)
             layer.iterate(ids_buf, gates_buf, Tg)       # counts come back to pinned host inside
             layer._last_gates = gates_buf
+        layer.sync_weights(stream)
         e2.record(stream)
         barrier()
         et = torch.tensor([s2.elapsed_time(e2) / Ke], device="cuda")
@@ -571,7 +573,8 @@ def gpu_arm(args, wl):
             "steps": K, "warmup": args.warmup, "ms_per_step": round(ms_iter, 4),
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (walk-spike routing trace, counter-hash grads)",
-            "config": dict(_config(wl, G), dedup=bool(args.dedup), host_state=bool(args.host_state),
+            "config": dict(_config(wl, G), dedup=bool(args.dedup), lazy_replicate=bool(args.lazy),
+                           host_state=bool(args.host_state),
                            policy=args.policy,
                            replan_interval=args.interval, capacity_factor=args.cf or None),
             "roofline": roof,
@@ -617,6 +620,8 @@ def main():
     ap.add_argument("--interval", type=int, default=1, help="re-place every i iterations (row f2)")
     ap.add_argument("--cf", type=float, default=0.0, help="capacity factor; 0 = drop-free (row f2)")
     ap.add_argument("--no-a2a", action="store_true", help="skip the row f3 token all-to-all timing")
+    ap.add_argument("--lazy", default="auto", choices=["auto", "on", "off"],
+                    help="defer de-dup's local replication to a library stream (auto: with de-dup)")
     ap.add_argument("--host-state", action="store_true",
                     help="row f4: optimizer shards in pinned host memory (MOE_OPT_HOST_STATE)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -629,6 +634,7 @@ def main():
     args.warmup = max(args.warmup, 0)
     # nothing crosses NVLink at G = 1 (the library ignores the option there too)
     args.dedup = args.gpus > 1 and args.dedup in ("auto", "on")
+    args.lazy = args.dedup and args.lazy in ("auto", "on")
     from synth import configs
     wl = configs.CONFIGS[args.config]
     if args.impl == "reference":

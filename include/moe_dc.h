@@ -160,6 +160,14 @@ typedef struct {
  * host memory (or, without the option, if they are not device memory).                */
 #define MOE_OPT_HOST_STATE 2
 
+/* With MOE_OPT_DEDUP: the local replication of the placed weights (each GPU copying an
+ * expert's first slot into its other slots of that expert) runs on a library stream instead
+ * of at the end of moe_update's stream work, so it overlaps whatever the caller enqueues next
+ * (the next iteration's dispatch does not read slot weights).  The library joins it before
+ * any later kernel that writes slot weights (moe_update, moe_place); the caller must call
+ * moe_ctx_weights_wait(ctx, stream) before `stream` reads slot weights.                    */
+#define MOE_OPT_LAZY_REPLICATE 4
+
 /* Creates a context (allocates scratch and the sync buffer on desc->device).
  * Virtual mode is ready immediately.  Real mode (G > 1) additionally needs
  * moe_ctx_export + an exchange of the handles between ranks + moe_ctx_connect.  */
@@ -208,6 +216,10 @@ int moe_ctx_check(moe_ctx *ctx, void *stream);
  * scatter kernel), so the host planner (step 6 may "execute earlier, even right after
  * step 1", PAPER.md:709 fn) overlaps the scatter.  MOE_OK if no dispatch was issued.  */
 int moe_ctx_wait_counts(moe_ctx *ctx);
+
+/* Makes `stream` wait until every slot weight of the last moe_update / moe_place is in place
+ * (only needed with MOE_OPT_LAZY_REPLICATE; otherwise a no-op).  Asynchronous.            */
+int moe_ctx_weights_wait(moe_ctx *ctx, void *stream);
 
 /* ------------------------------------------------------------------------------------------
  * a0 + a2 Dispatch -- device, asynchronous on `stream`; collective across GPUs in real mode

@@ -22,7 +22,7 @@ EXPORTED = [
     "moe_status_str", "moe_last_error", "moe_abi_version", "moe_plan", "moe_plan_ex",
     "moe_slot_capacity",
     "moe_ctx_create", "moe_ctx_destroy", "moe_ctx_handle_bytes", "moe_ctx_export",
-    "moe_ctx_connect", "moe_ctx_check", "moe_ctx_wait_counts", "moe_dispatch", "moe_update",
+    "moe_ctx_connect", "moe_ctx_check", "moe_ctx_wait_counts", "moe_ctx_weights_wait", "moe_dispatch", "moe_update",
     "moe_place", "moe_step", "moe_ctx_set_timing", "moe_ctx_get_timing", "moe_ctx_get_timing_ex",
     "moe_synth_grads", "moe_synth_master",
     "moe_tokx_create", "moe_tokx_destroy", "moe_tokx_handle_bytes", "moe_tokx_export",
@@ -51,6 +51,7 @@ class MoeCtxDesc(C.Structure):
 
 MOE_OPT_DEDUP = 1
 MOE_OPT_HOST_STATE = 2
+MOE_OPT_LAZY_REPLICATE = 4
 
 
 class MoeDispatchOut(C.Structure):
@@ -102,6 +103,8 @@ def lib() -> C.CDLL:
         L.moe_ctx_check.argtypes = [C.c_void_p, C.c_void_p]
         L.moe_ctx_wait_counts.restype = C.c_int
         L.moe_ctx_wait_counts.argtypes = [C.c_void_p]
+        L.moe_ctx_weights_wait.restype = C.c_int
+        L.moe_ctx_weights_wait.argtypes = [C.c_void_p, C.c_void_p]
         L.moe_place.restype = C.c_int
         L.moe_place.argtypes = [C.c_void_p, C.POINTER(MoePlanT), C.c_void_p]
         L.moe_dispatch.restype = C.c_int

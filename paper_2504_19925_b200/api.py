@@ -13,7 +13,7 @@ import numpy as np
 import torch
 
 from . import _lib as L
-from ._lib import (MOE_OPT_DEDUP, MOE_OPT_HOST_STATE, MOE_PLAN_KEEP, MOE_PLAN_MINMAX, MOE_PLAN_PAPER_ALG1,  # noqa: F401
+from ._lib import (MOE_OPT_DEDUP, MOE_OPT_HOST_STATE, MOE_OPT_LAZY_REPLICATE, MOE_PLAN_KEEP, MOE_PLAN_MINMAX, MOE_PLAN_PAPER_ALG1,  # noqa: F401
                    MOE_PLAN_STATIC, MoeError, check)
 
 
@@ -169,6 +169,11 @@ class MoeContext:
                 "n_update_kernel": n[1], "presum_ms": ms[2], "n_presum": n[2],
                 "replicate_ms": ms[3], "n_replicate": n[3], "update_ms": ms[4], "n_update": n[4],
                 "host_wait_ms": ms[5], "n_host_wait": n[5], "host_plan_ms": ms[6], "n_host_plan": n[6]}
+
+    def weights_wait(self, stream=None) -> None:
+        """`stream` waits until every slot weight of the last update/place is in place (only
+        matters with MOE_OPT_LAZY_REPLICATE)."""
+        check(L.lib().moe_ctx_weights_wait(self.handle, _stream_ptr(stream)), "moe_ctx_weights_wait")
 
     def wait_counts(self) -> None:
         """Host waits for the C_e copy of the last moe_dispatch (not for its scatter)."""

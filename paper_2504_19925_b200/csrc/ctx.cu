@@ -82,6 +82,9 @@ void free_ctx(moe_ctx *c) {
   for (float *p : c->presum) cudaFree(p);
   if (c->side) cudaStreamDestroy(c->side);
   if (c->hi) cudaStreamDestroy(c->hi);
+  if (c->repl) cudaStreamDestroy(c->repl);
+  if (c->ev_repl_in) cudaEventDestroy(c->ev_repl_in);
+  if (c->ev_repl_done) cudaEventDestroy(c->ev_repl_done);
   if (c->ev_hi_in) cudaEventDestroy(c->ev_hi_in);
   if (c->ev_hi_out) cudaEventDestroy(c->ev_hi_out);
   if (c->ev_side_start) cudaEventDestroy(c->ev_side_start);
@@ -291,6 +294,12 @@ extern "C" int moe_ctx_create(const moe_ctx_desc *d, moe_ctx **out) {
     if (se == cudaSuccess) se = cudaStreamCreateWithPriority(&c->hi, cudaStreamNonBlocking, greatest);
     if (se == cudaSuccess) se = cudaEventCreateWithFlags(&c->ev_hi_in, cudaEventDisableTiming);
     if (se == cudaSuccess) se = cudaEventCreateWithFlags(&c->ev_hi_out, cudaEventDisableTiming);
+    c->lazy_repl = (d->options & MOE_OPT_LAZY_REPLICATE) != 0;
+    if (c->lazy_repl) {
+      if (se == cudaSuccess) se = cudaStreamCreateWithFlags(&c->repl, cudaStreamNonBlocking);
+      if (se == cudaSuccess) se = cudaEventCreateWithFlags(&c->ev_repl_in, cudaEventDisableTiming);
+      if (se == cudaSuccess) se = cudaEventCreateWithFlags(&c->ev_repl_done, cudaEventDisableTiming);
+    }
     if (se == cudaSuccess) se = cudaEventCreateWithFlags(&c->ev_side_start, cudaEventDisableTiming);
     if (se == cudaSuccess) se = cudaEventCreateWithFlags(&c->ev_presum_done, cudaEventDisableTiming);
     if (se != cudaSuccess) {
@@ -400,6 +409,14 @@ int moe_hi_end(moe_ctx *ctx, void *hi, void *stream) {
   if (hi == stream) return MOE_OK;
   MOE_CUDA_TRY(cudaEventRecord(ctx->ev_hi_out, (cudaStream_t)hi));
   MOE_CUDA_TRY(cudaStreamWaitEvent((cudaStream_t)stream, ctx->ev_hi_out, 0));
+  return MOE_OK;
+}
+
+extern "C" int moe_ctx_weights_wait(moe_ctx *ctx, void *stream) {
+  if (!ctx) return fail(MOE_ERR_INVALID, "moe_ctx_weights_wait: NULL ctx");
+  if (!ctx->repl_pending) return MOE_OK;
+  MOE_CUDA_TRY(cudaSetDevice(ctx->device));
+  MOE_CUDA_TRY(cudaStreamWaitEvent((cudaStream_t)stream, ctx->ev_repl_done, 0));
   return MOE_OK;
 }
 

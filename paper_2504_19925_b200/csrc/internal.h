@@ -90,6 +90,10 @@ struct moe_ctx {
   std::vector<float *> presum; // [n_local] library-owned
   cudaStream_t side;           // stream for the early k_presum (moe_step)
   cudaStream_t hi;             // highest-priority stream for moe_step's dispatch kernels
+  bool lazy_repl;              // MOE_OPT_LAZY_REPLICATE: k_replicate on `repl`, joined lazily
+  bool repl_pending;
+  cudaStream_t repl;
+  cudaEvent_t ev_repl_in, ev_repl_done;
   cudaEvent_t ev_hi_in, ev_hi_out;
   cudaEvent_t ev_side_start, ev_presum_done;
   bool presum_ready;           // a k_presum for plan presum_fs is in flight on `side`

@@ -745,6 +745,10 @@ int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *pl
     return fail(MOE_ERR_INVALID, "moe_update/moe_place: real-mode context not connected");
   MOE_CUDA_TRY(cudaSetDevice(ctx->device));
   cudaStream_t s = (cudaStream_t)stream;
+  if (ctx->repl_pending) {  // the previous lazy k_replicate writes slot weights too
+    MOE_CUDA_TRY(cudaStreamWaitEvent(s, ctx->ev_repl_done, 0));
+    ctx->repl_pending = false;
+  }
 
   UpdArgs a{};
   a.E = ctx->E;
@@ -963,10 +967,20 @@ int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *pl
     if (nsrc > 0) {
       const int gx = std::max(1, std::min<int>((int)((ctx->P - ctx->Pg) / (kThreads * kVec)) + 1,
                                                8 * ctx->num_sms / nsrc + 1));
-      const auto rev = timing_begin(ctx, s);
-      k_replicate<<<dim3(gx, ctx->n_local * ctx->S), kThreads, 0, s>>>(ra);
+      cudaStream_t rs = s;
+      if (ctx->lazy_repl) {  // off the caller's stream; joined before the next slot-weight writer
+        MOE_CUDA_TRY(cudaEventRecord(ctx->ev_repl_in, s));
+        MOE_CUDA_TRY(cudaStreamWaitEvent(ctx->repl, ctx->ev_repl_in, 0));
+        rs = ctx->repl;
+      }
+      const auto rev = timing_begin(ctx, rs);
+      k_replicate<<<dim3(gx, ctx->n_local * ctx->S), kThreads, 0, rs>>>(ra);
       MOE_CUDA_TRY(cudaGetLastError());
-      timing_end(ctx->ev_repl, rev, s);
+      timing_end(ctx->ev_repl, rev, rs);
+      if (ctx->lazy_repl) {
+        MOE_CUDA_TRY(cudaEventRecord(ctx->ev_repl_done, rs));
+        ctx->repl_pending = true;
+      }
     }
   }
   timing_end(ctx->ev_stage, stage_ev, s);

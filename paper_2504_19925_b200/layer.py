@@ -24,12 +24,16 @@ class DecoupledExpertLayer:
                  device: int | None = None, seed: int = 0, adam: api.AdamConfig | None = None,
                  policy: int = api.MOE_PLAN_PAPER_ALG1, scale_mode: int = 0, scale=None,
                  init_master: bool = True, dedup: bool = False, capacity: int = 0,
-                 replan_interval: int = 1, host_state: bool = False):
+                 replan_interval: int = 1, host_state: bool = False,
+                 lazy_replicate: bool = False):
         """capacity > 0 (per-replica slot capacity, see api.moe_slot_capacity) and
         replan_interval > 1 (re-place only every i iterations; MOE_PLAN_STATIC for the static
         baseline) are row f2 (readings B1-B3); the defaults are the paper's drop-free,
         per-iteration path.  host_state=True (row f4, MOE_OPT_HOST_STATE) keeps the fp32
-        master/m/v shards in pinned host memory; the update streams them over PCIe."""
+        master/m/v shards in pinned host memory; the update streams them over PCIe.
+        lazy_replicate=True (with dedup, MOE_OPT_LAZY_REPLICATE) lets the local replication of
+        the placed weights overlap the next iteration; call sync_weights() before reading
+        slot_w."""
         if replan_interval < 1:
             raise ValueError("replan_interval must be >= 1")
         self.replan_interval = replan_interval
@@ -59,7 +63,8 @@ class DecoupledExpertLayer:
         self.adam_m = [state(True) for _ in range(n)]
         self.adam_v = [state(True) for _ in range(n)]
         self.host_state = host_state
-        opts = (api.MOE_OPT_DEDUP if dedup else 0) | (api.MOE_OPT_HOST_STATE if host_state else 0)
+        opts = ((api.MOE_OPT_DEDUP if dedup else 0) | (api.MOE_OPT_HOST_STATE if host_state else 0) |
+                (api.MOE_OPT_LAZY_REPLICATE if lazy_replicate else 0))
         self.ctx = api.MoeContext(E, G, S, k, P, max_tokens, rank, self.slot_w, self.slot_g,
                                   self.master, self.adam_m, self.adam_v, device=device,
                                   options=opts)
@@ -117,6 +122,10 @@ class DecoupledExpertLayer:
         self.plan = nxt
         self.t += 1
         return nxt
+
+    def sync_weights(self, stream=None) -> None:
+        """Make `stream` (default: current) wait until slot_w holds every weight of self.plan."""
+        self.ctx.weights_wait(stream)
 
     def close(self) -> None:
         self.ctx.close()

@@ -17,7 +17,7 @@ def run_parity(name: str, G: int, iters: int, *, rank_mode: str = "virtual", idx
                T: int | None = None, policy: int = 0, scale_mode: int = 0, scale=None,
                weight_decay: float = 0.0, trace=None, check_dispatch: bool = True,
                dedup: bool = False, capacity: int = 0, replan_interval: int = 1,
-               host_state: bool = False):
+               host_state: bool = False, lazy_replicate: bool = False):
     """Returns the number of iterations compared.  rank_mode: "virtual" (rank=-1, G ranks on
     cuda:0) or "single" (real mode with G == 1)."""
     from paper_2504_19925_b200 import AdamConfig, DecoupledExpertLayer
@@ -39,7 +39,7 @@ def run_parity(name: str, G: int, iters: int, *, rank_mode: str = "virtual", idx
     layer = DecoupledExpertLayer(E, G, S, k, P, Tg, rank=rank, device=0, seed=seed, adam=adam,
                                  policy=policy, scale_mode=scale_mode, scale=scale, dedup=dedup,
                                  capacity=capacity, replan_interval=replan_interval,
-                                 host_state=host_state)
+                                 host_state=host_state, lazy_replicate=lazy_replicate)
     pol = {0: "alg1", 1: "minmax", 2: "static"}[policy]
     idx_arr = np.arange(P, dtype=np.int64) if idx is None else np.asarray(idx, dtype=np.int64)
     sim = ostep.OracleSim(E, G, S, P, seed, hyper=hyper, policy=pol, scale_mode=scale_mode,
@@ -102,6 +102,7 @@ def run_parity(name: str, G: int, iters: int, *, rank_mode: str = "virtual", idx
 
 
 def _compare_weights(layer, sim, idx_t, G, S, P, t=-1):
+    layer.sync_weights()
     for v in range(G):
         w = layer.slot_w[v].view(torch.int16).view(S, P)[:, idx_t].cpu().numpy().view(np.uint16)
         want = sim.w_slot[v * S:(v + 1) * S]

@@ -32,6 +32,7 @@ def main() -> int:
     ap.add_argument("--policy", type=int, default=0, help="0 alg1, 1 minmax, 2 static")
     ap.add_argument("--interval", type=int, default=1, help="re-placement interval (row f2)")
     ap.add_argument("--host-state", action="store_true", help="row f4: state in pinned host memory")
+    ap.add_argument("--lazy", action="store_true", help="MOE_OPT_LAZY_REPLICATE (with --dedup)")
     ap.add_argument("--tokens", type=int, default=-1,
                     help="row f3: also run the token dispatch/combine with these flags (0 or 1)")
     args = ap.parse_args()
@@ -56,7 +57,8 @@ def main() -> int:
     cap = slot_capacity(args.cf, wl.T, k, G * S) if args.cf > 0 else 0
     layer = DecoupledExpertLayer(E, G, S, k, P, Tg, rank=rank, device=local, seed=seed,
                                  dedup=args.dedup, capacity=cap, policy=args.policy,
-                                 replan_interval=args.interval, host_state=args.host_state)
+                                 replan_interval=args.interval, host_state=args.host_state,
+                                 lazy_replicate=args.lazy)
     layer.connect()
     tx = None
     if args.tokens >= 0:
@@ -106,6 +108,7 @@ def main() -> int:
             msgs.append(what)
 
     def check_weights(t):
+        layer.sync_weights()
         w = layer.slot_w[0].view(torch.int16).view(S, P)[:, idx_t].cpu().numpy().view(np.uint16)
         expect(np.array_equal(w, sim.w_slot[rank * S:(rank + 1) * S]), f"iter {t}: slot weights")
 

@@ -85,10 +85,13 @@ def test_edge_cases_empty_and_degenerate():
                                                   ("medium", 2, 4, False), ("gpt-small", 8, 2, True)])
 def test_dedup_is_bit_identical(name, G, iters, sampled):
     """Locality de-duplication (row f1): local fp32 partials + once-per-GPU pushes +
-    local replication give exactly the oracle's bits (reading A11 makes them identical)."""
+    local replication give exactly the oracle's bits (reading A11 makes them identical);
+    also with the replication deferred to its own stream (MOE_OPT_LAZY_REPLICATE)."""
     from gpu_helpers import run_parity
     wl = configs.CONFIGS[name]
     run_parity(name, G, iters, dedup=True, idx=_sample_idx(wl.P, G) if sampled else None)
+    if not sampled:
+        run_parity(name, G, iters, dedup=True, lazy_replicate=True)
 
 
 @pytest.mark.parametrize("name,G,cf", [("tiny-skew", 4, 1.0), ("tiny-odd", 3, 0.5), ("medium", 4, 1.25),

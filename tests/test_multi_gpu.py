@@ -38,6 +38,7 @@ def _torchrun(n: int, *args, timeout=600):
     (2, "tiny", ["--tokens", "1"]), (4, "medium", ["--tokens", "0", "--cf", "1.25", "--iters", "3"]),
     (4, "tiny-skew", ["--tokens", "1", "--dedup", "--trace", "rotating-hot"]),
     (4, "medium", ["--host-state", "--dedup", "--iters", "4"]), (2, "medium", ["--host-state", "--iters", "3"]),
+    (4, "medium", ["--dedup", "--lazy", "--iters", "4"]), (2, "tiny-skew", ["--dedup", "--lazy", "--tokens", "1"]),
 ], ids=lambda x: "".join(a.lstrip("-") for a in x) if isinstance(x, list) else str(x))
 def test_real_multi_gpu_parity(G, config, extra):
     if torch.cuda.device_count() < G:
