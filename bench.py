@@ -285,7 +285,7 @@ def measure_pcie(device: int, nbytes: int = 1 << 30) -> dict:
 # ------------------------------------------------------------------------------------------
 # Row f3: token all-to-all along the last iteration's routing
 # ------------------------------------------------------------------------------------------
-def token_a2a(args, wl, layer, G, rank, Tg, S, peak_hbm, barrier, stream):
+def token_a2a(args, wl, layer, gates, G, rank, Tg, S, peak_hbm, barrier, stream):
     """Times the forward pair -- moe_token_dispatch (plain copy) and moe_token_combine
     (gate-weighted) -- on the
     routing of the last timed iteration: bf16 activations [T_g][d] -> expert buffers ->
@@ -313,7 +313,6 @@ def token_a2a(args, wl, layer, G, rank, Tg, S, peak_hbm, barrier, stream):
     g = torch.Generator(device="cuda").manual_seed(1234 + rank)
     src = torch.randn(Tg * d, device="cuda", generator=g).to(torch.bfloat16)
     dst = torch.empty(Tg * d, dtype=torch.bfloat16, device="cuda")
-    gates = layer._last_gates
     K = max(3, min(args.steps, 20))
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
     for _ in range(2):  # warm-up
@@ -410,12 +409,13 @@ def gpu_arm(args, wl):
     stream = torch.cuda.current_stream()
 
     plans = []  # (first_slot of plan_t, of plan_t+1) per timed step, for the byte accounting
+    last_gates = [None]  # gates of the last iterated step (the routing layer.out holds)
 
     def step(i, record=False):
         t = i % n_tr
         cur = layer.plan.first_slot.copy() if record else None
         nxt = layer.iterate(ids_d[t], gates_d[t], Tg)  # moe_step: a0+a2 -> a1 (host) -> a3+a4+a5
-        layer._last_gates = gates_d[t]
+        last_gates[0] = gates_d[t]
         if record:
             plans.append((cur, nxt.first_slot.copy()))
 
@@ -491,7 +491,7 @@ def gpu_arm(args, wl):
             gates_buf.copy_(gates_h[tt], non_blocking=True)
             layer.slot_g[0].copy_(grads_h, non_blocking=True)
             layer.iterate(ids_buf, gates_buf, Tg)       # counts come back to pinned host inside
-            layer._last_gates = gates_buf
+            last_gates[0] = gates_buf
         layer.sync_weights(stream)
         e2.record(stream)
         barrier()
@@ -559,7 +559,8 @@ def gpu_arm(args, wl):
     # our kernels launched in the timed region, from the library's own launch counters
     n_launch = 3 * tm["n_dispatch"] + tm["n_update_kernel"] + tm["n_presum"] + tm["n_replicate"]
 
-    a2a = None if args.no_a2a else token_a2a(args, wl, layer, G, rank, Tg, S, peak_hbm, barrier, stream)
+    a2a = None if args.no_a2a else token_a2a(args, wl, layer, last_gates[0], G, rank, Tg, S, peak_hbm,
+                                               barrier, stream)
 
     cpu = None
     if rank == 0 and G == 1 and not args.no_cpu_baseline:

@@ -48,6 +48,8 @@ typedef struct moe_tokx moe_tokx;
  * Real mode with G > 1: every rank then calls moe_tokx_export and moe_tokx_connect with all
  * ranks' records (like moe_ctx_connect).  MOE_ERR_INVALID on bad sizes or NULL pointers.  */
 int moe_tokx_create(moe_ctx *ctx, int64_t d, int64_t rows, void *const *xbuf, moe_tokx **out);
+/* The context must outlive the token exchange: destroy the exchange first (destroy itself
+ * does not touch the context).                                                           */
 int moe_tokx_destroy(moe_tokx *x);
 int moe_tokx_handle_bytes(void);
 int moe_tokx_export(moe_tokx *x, void *out);           /* writes moe_tokx_handle_bytes() */

@@ -129,6 +129,7 @@ class MoeContext:
         desc = L.MoeCtxDesc(E, G, S, k, P, max_tokens, rank, self.device,
                             *[C.cast(a, C.POINTER(C.c_void_p)) for a in self._arrs], options)
         self.options = options
+        self._children = []  # objects bound to this context (token exchanges): closed first
         h = C.c_void_p()
         check(L.lib().moe_ctx_create(C.byref(desc), C.byref(h)), "moe_ctx_create")
         self._h = h
@@ -183,6 +184,10 @@ class MoeContext:
         check(L.lib().moe_ctx_check(self.handle, _stream_ptr(stream)), "moe_ctx_check")
 
     def close(self) -> None:
+        for ref in getattr(self, "_children", []):
+            child = ref()
+            if child is not None:
+                child.close()
         if getattr(self, "_h", None) is not None:
             L.lib().moe_ctx_destroy(self._h)
             self._h = None
@@ -322,6 +327,8 @@ class TokenExchange:
         h = C.c_void_p()
         check(L.lib().moe_tokx_create(ctx.handle, d, rows, self._arr, C.byref(h)), "moe_tokx_create")
         self._h = h
+        import weakref
+        ctx._children.append(weakref.ref(self))  # the context closes us before itself
 
     @property
     def handle(self) -> C.c_void_p:

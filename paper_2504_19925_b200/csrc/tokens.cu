@@ -56,7 +56,8 @@ constexpr int kCombU = 2;  // combine: vectors per lane per row chunk, two rows 
 }  // namespace
 
 struct moe_tokx {
-  moe_ctx *ctx;
+  moe_ctx *ctx;    // must outlive this object (destroy the token exchange first)
+  int device;
   int64_t d, rows, dv;  // dv = d / 8 vectors per row
   std::vector<void *> xbuf;                  // [n_local] caller buffers
   void *peer_xbuf[MOE_MAX_G];
@@ -403,6 +404,7 @@ extern "C" int moe_tokx_create(moe_ctx *ctx, int64_t d, int64_t rows, void *cons
   MOE_CUDA_TRY(cudaSetDevice(ctx->device));
   moe_tokx *x = new moe_tokx();
   x->ctx = ctx;
+  x->device = ctx->device;
   x->d = d;
   x->rows = rows;
   x->dv = d / 8;
@@ -440,7 +442,7 @@ extern "C" int moe_tokx_create(moe_ctx *ctx, int64_t d, int64_t rows, void *cons
 
 extern "C" int moe_tokx_destroy(moe_tokx *x) {
   if (!x) return MOE_OK;
-  cudaSetDevice(x->ctx->device);
+  cudaSetDevice(x->device);  // (does not touch the context)
   for (auto &kv : x->opened) cudaIpcCloseMemHandle(kv.second);
   cudaFree(x->sync);
   delete x;

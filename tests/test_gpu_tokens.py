@@ -159,3 +159,13 @@ def test_special_values_bitwise():
     layer.ctx.check()
     tx.close()
     layer.close()
+
+
+def test_context_close_closes_token_exchange_first():
+    """Closing the context first must not leave a dangling token exchange (use-after-free)."""
+    from paper_2504_19925_b200 import DecoupledExpertLayer, TokenExchange
+    layer = DecoupledExpertLayer(8, 1, 8, 2, 64, 16, rank=0, device=0)
+    tx = TokenExchange(layer.ctx, 16, 4)
+    layer.close()                      # closes tx, then the context
+    assert tx._h is None
+    tx.close()                         # idempotent
