@@ -203,3 +203,18 @@ def test_alg1_is_not_minmax_counterexample(golden_dir):
     assert best == ex["optimal_max_load"]
     rm = P.minmax(c, 4, 1, ex["slots_total"])
     assert max(-(-int(c[e]) // int(rm[e])) for e in range(4)) == ex["optimal_max_load"]
+
+
+def test_alg1_ties_lowest_index_hand_derived():
+    """Reading A2 ("argmax/argmin tie-breaking: lowest index wins"), derived by
+    hand from the listing:
+    * [1,1,1,1] on 6 slots: goal 1.5 each -> r = [1,1,1,1], diff -0.5 each; the
+      under-allocation loop takes argmin twice: index 0, then index 1 -> [2,2,1,1].
+    * [0,0,5,5] on 5 slots: goal [0,0,2.5,2.5] -> r = [1,1,2,2] (sum 6), diff [1,1,-.5,-.5];
+      over-allocation picks 0 and 1 (clamped at 1: only diff drops, to 0), again 0 and 1
+      (diff -1), then 2 (tie with 3): r[2] = 1 -> [1,1,1,2] after 5 steps.
+    Highest-index tie-breaking would give [1,1,2,2] and [1,1,2,1]."""
+    r, steps = P.alg1(np.array([1, 1, 1, 1]), 4, 1, 6, return_steps=True)
+    assert r.tolist() == [2, 2, 1, 1] and steps == (0, 2)
+    r, steps = P.alg1(np.array([0, 0, 5, 5]), 4, 1, 5, return_steps=True)
+    assert r.tolist() == [1, 1, 1, 2] and steps == (5, 0)
