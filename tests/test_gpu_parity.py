@@ -226,7 +226,8 @@ def test_full_size_sampled(name, G, iters):
     every slot (the oracle computes them one by one)."""
     from gpu_helpers import run_parity
     wl = configs.CONFIGS[name]
-    run_parity(name, G, iters, idx=_sample_idx(wl.P, G))
+    # G = 1 exactly as bench.py launches it (real mode, rank 0); G > 1 in virtual mode
+    run_parity(name, G, iters, idx=_sample_idx(wl.P, G), rank_mode="single" if G == 1 else "virtual")
 
 
 @pytest.mark.parametrize("policy,interval", [("alg1", 1), ("alg1", 10), ("static", 1)])
