@@ -102,8 +102,9 @@ def update_stage_bytes(fs_cur, fs_next, G: int, S: int, P: int, E: int, dedup: b
     writes its bf16 slice into every next-plan slot of e; GPU g also reads+writes its
     master/m/v (24 B/element).  At G = 1 this is 2*S*P + 24*E*P + 2*S*P, and the NVLink bytes
     per direction are 4*S*(G-1)/G*P for ANY placement (App. E).
-    De-dup (row f1): a GPU with r >= 3 replicas of e first reads them (2rP) and writes an fp32
-    partial (4P) that owners then read (4 B/element); a remote GPU receives each shard once
+    De-dup (row f1): a GPU with r >= 3 replicas of e first reads them and writes an fp32
+    partial over the OTHER owners' ranges ((2r+4)(P-Pg)), which those owners then read
+    (4 B/element; the local owner reads its slices); a remote GPU receives each shard once
     and copies it into its other slots of e (read + write of the remote owners' ranges).
     host_state (row f4): the 24 B/element of master/m/v cross PCIe instead (12 B each way),
     reported as "pcie_per_dir"; the HBM bytes drop them.
@@ -118,10 +119,10 @@ def update_stage_bytes(fs_cur, fs_next, G: int, S: int, P: int, E: int, dedup: b
             if r <= 0:
                 continue
             partial = dedup and r >= 3
-            if partial:
-                pre[h] += 2 * r * P + 4 * P
-            per_owner = 4 * Pg if partial else 2 * r * Pg
+            if partial:  # partials over the remote owners' ranges only
+                pre[h] += (2 * r + 4) * (P - Pg)
             for g in range(G):
+                per_owner = 4 * Pg if (partial and g != h) else 2 * r * Pg  # own range: slices
                 upd[h] += per_owner
                 if g != h:
                     nout[h] += per_owner

@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_update_tma(const __grid_cons
       const int j0 = a.fs_cur[e], j1 = a.fs_cur[e + 1];
       for (int h = a.h_first_cur[e], ja = j0; ja < j1; ++h) {  // GPU h's run [ja, jb) of e's slots
         const int jb = min(j1, (h + 1) * a.S);
-        const int q = a.dedup ? a.pq[e][h] : -1;
+        const int q = (a.dedup && h != o) ? a.pq[e][h] : -1;  // own GPU: read the slices
         if (q >= 0) {  // de-dup: GPU h's fp32 partial of this run, as two 4 KB ring slots
           const float *src = a.presum[h] + (int64_t)q * P + g0;
           const uint32_t nA = nval < kChunk / 2 ? nval : kChunk / 2, nB = nval - nA;
@@ -458,7 +458,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_update_tma(const __grid_cons
     bool have_tot = false;
     for (int h = a.h_first_cur[e], ja = j0; ja < j1; ++h) {
       const int jb = min(j1, (h + 1) * a.S);
-      const int q = a.dedup ? a.pq[e][h] : -1;
+      const int q = (a.dedup && h != o) ? a.pq[e][h] : -1;
       if (q >= 0) {
         const int gA = gi_ % kGradSlots, gB = (gi_ + 1) % kGradSlots;
         mbar_wait(gr_full + gA, (gi_ / kGradSlots) & 1);
@@ -563,7 +563,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_update_tma(const __grid_cons
 // ------------------------------------------------------------------------------------------
 struct PresumArgs {
   int32_t S, o_begin, nq_total;
-  int64_t P, nchunks;                 // kChunk-element chunks over the full [0, P)
+  int64_t P, Pg, nchunks;             // kChunk-element chunks over the full [0, P)
   int32_t qoff[MOE_MAX_G + 1];        // prefix of partial rows over local ranks
   int16_t q_e[MOE_MAX_G][MOE_MAX_E];  // expert of partial row q of local rank v
   int32_t fs[MOE_MAX_E + 1];          // plan_cur
@@ -582,6 +582,9 @@ __global__ void __launch_bounds__(kThreads) k_presum(const __grid_constant__ Pre
     const int e = a.q_e[v][q];
     const int h = a.o_begin + v;
     const int ja = max(a.fs[e], h * a.S), jb = min(a.fs[e + 1], (h + 1) * a.S);
+    // the GPU's own owner range is never read as a partial (its owner reads the local slices
+    // directly, the same bits by A11): skip chunks entirely inside [h*Pg, (h+1)*Pg)
+    if (c * kChunk >= (int64_t)h * a.Pg && (c + 1) * kChunk <= (int64_t)(h + 1) * a.Pg) continue;
     const int64_t i = c * kChunk + (int64_t)threadIdx.x * kVec;
     if (i >= a.P) continue;
     const uint16_t *base = a.grads[v] + i;
@@ -713,6 +716,7 @@ int build_presum(moe_ctx *ctx, const moe_plan_t *plan_cur, int8_t (&pq)[MOE_MAX_
   pa.S = ctx->S;
   pa.o_begin = o_begin;
   pa.P = ctx->P;
+  pa.Pg = ctx->Pg;
   pa.nchunks = (ctx->P + kChunk - 1) / kChunk;
   for (int e = 0; e <= ctx->E; ++e) pa.fs[e] = plan_cur->first_slot[e];
   for (int h = 0; h < ctx->G; ++h) {
