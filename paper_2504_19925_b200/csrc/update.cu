@@ -254,16 +254,22 @@ __global__ void __launch_bounds__(kThreads) k_update(const __grid_constant__ Upd
 //   warps 0-7 (consumers, 8 elements per thread): wait full -> read smem -> arrive empty;
 //     the same two-level sum / Adam / bf16 as k_update, then 16-byte stores of the state
 //     and of the bf16 weights to every slot of plan_next (local or peer HBM).
-// 2 CTAs per SM (~97 KB shared memory each).
+// 2 CTAs per SM (~113 KB shared memory each).
 // ------------------------------------------------------------------------------------------
 constexpr int kConsumerWarps = kThreads / 32;            // 8
 constexpr int kTmaThreads = kThreads + 32;               // + 1 producer warp
 constexpr int kStateSlots = 2;
-constexpr int kGradSlots = 12;
 constexpr int kStateTileBytes = 3 * kChunk * 4;          // 24 KB
 constexpr int kGradTileBytes = kChunk * 2;               // 4 KB
-constexpr int kTmaSmem = kStateSlots * kStateTileBytes + kGradSlots * kGradTileBytes +
-                         2 * (kStateSlots + kGradSlots) * 8 + kStateSlots * 8;  // + slot item ids
+// grad ring depth: 16 x 4 KB (same-box A/B: 1 % faster than 12 at N = 1, equal at N = 4;
+// 2 CTAs x 112 KB still fit an SM)
+constexpr int kGradSlots = 16;
+template <int kGradSlots>
+constexpr int tma_smem() {
+  return kStateSlots * kStateTileBytes + kGradSlots * kGradTileBytes + 2 * (kStateSlots + kGradSlots) * 8 +
+         kStateSlots * 8;  // + slot item ids
+}
+
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -306,6 +312,7 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       : "memory");
 }
 
+template <int kGradSlots>
 __global__ void __launch_bounds__(kTmaThreads, 2) k_update_tma(const __grid_constant__ UpdArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   float *state = reinterpret_cast<float *>(smem);                              // [slots][3][chunk]
@@ -697,8 +704,8 @@ int moe_validate_plan(const moe_ctx *ctx, const moe_plan_t *p, const char *what)
 // Per-device setup at context creation: occupancy of k_update, shared-memory opt-in of
 // k_update_tma.  Returns blocks per SM of k_update (>= 1), or -1 on a CUDA error.
 int moe_update_init() {
-  if (cudaFuncSetAttribute(k_update_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem) !=
-      cudaSuccess)
+  if (cudaFuncSetAttribute(k_update_tma<kGradSlots>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           tma_smem<kGradSlots>()) != cudaSuccess)
     return -1;
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_update, kThreads, 0) != cudaSuccess) return -1;
@@ -881,7 +888,7 @@ int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *pl
       const int64_t grid = std::min<int64_t>(items, (int64_t)ctx->num_sms * 2);
       if (grid > 0) {
         const auto tev = timing_begin(ctx, s);
-        k_update_tma<<<(unsigned)grid, kTmaThreads, kTmaSmem, s>>>(ka);
+        k_update_tma<kGradSlots><<<(unsigned)grid, kTmaThreads, tma_smem<kGradSlots>(), s>>>(ka);
         MOE_CUDA_TRY(cudaGetLastError());
         timing_end(ctx->ev_upd, tev, s);
       }
