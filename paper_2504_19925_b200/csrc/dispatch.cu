@@ -202,10 +202,7 @@ __global__ void __launch_bounds__(kThreads) k_scan(const __grid_constant__ ScanA
   const int32_t q = C / r, m = C % r;
   const int32_t capv = a.cap > 0 ? a.cap : 0x7fffffff;
   const int GS = a.G * a.S;
-  if (v == 0 && tid == 0) {
-    a.counts_dev[e] = C;
-    if (a.counts_host) a.counts_host[e] = C;  // straight to pinned host memory (PCIe write)
-  }
+  if (v == 0 && tid == 0) a.counts_dev[e] = C;  // the last block copies all of them to the host
   // Per replica rho: load q or q+1, kept min(load, cap) (row f2), this rank's kept pairs in it
   // (send_count) and their exclusive prefix over rho (kept_pre: where the replica's kept pairs
   // start in this rank's slot-major order of e).
@@ -260,12 +257,23 @@ __global__ void __launch_bounds__(kThreads) k_scan(const __grid_constant__ ScanA
     run += c;
   }
 
-  // The last block publishes "C_t is on the host" (threadfence-reduction pattern): every
-  // block orders its host writes before its ticket; the last one releases the host flag.
+  // The last block publishes C_t to the host (threadfence-reduction pattern): every block
+  // orders its counts_dev write before its ticket (GPU scope); the last one copies the E
+  // counts to pinned host memory and releases the host flag -- one system-scope fence per
+  // dispatch instead of one per expert (it was ~40 % of this kernel's stall samples).
+  __shared__ int s_last;
   __syncthreads();
   if (tid == 0) {
-    __threadfence_system();
-    if (atomicAdd(a.scan_done, 1u) == gridDim.x * gridDim.y - 1) {
+    __threadfence();
+    s_last = atomicAdd(a.scan_done, 1u) == gridDim.x * gridDim.y - 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    if (a.counts_host)
+      for (int x = tid; x < a.E; x += kThreads) a.counts_host[x] = __ldcg(a.counts_dev + x);
+    __syncthreads();
+    if (tid == 0) {
       *a.scan_done = 0;
       __threadfence_system();
       st_release_sys(a.host_flag, a.epoch);
