@@ -104,11 +104,14 @@ __global__ void __launch_bounds__(kThreads) k_hist(const __grid_constant__ HistA
       a.dst[0]->xcnt[a.parity][grank][e] = c;
     }
   }
-  __threadfence_system();
+  // peers (real mode, G > 1) acquire the counts through a system-scope flag; on one GPU the
+  // dependent k_scan's griddepcontrol.wait already orders them
+  const bool flags = a.real && a.G > 1;
+  if (flags) __threadfence_system();
   __syncthreads();
   if (tid == 0) {
     a.done[v] = 0;
-    if (a.real)
+    if (flags)
       for (int h = 0; h < a.G; ++h) st_release_sys(&a.dst[h]->disp_flag[grank], a.epoch);
   }
 }
@@ -175,7 +178,7 @@ __global__ void __launch_bounds__(kThreads) k_scan(const __grid_constant__ ScanA
 
   if (tid == 0) {
     ok = 1;
-    if (a.real)
+    if (a.real && a.G > 1)
       for (int h = 0; h < a.G; ++h)
         if (!wait_flag(&a.sync->disp_flag[h], a.epoch, a.err)) ok = 0;
   }
