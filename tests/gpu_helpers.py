@@ -17,19 +17,21 @@ def run_parity(name: str, G: int, iters: int, *, rank_mode: str = "virtual", idx
                T: int | None = None, policy: int = 0, scale_mode: int = 0, scale=None,
                weight_decay: float = 0.0, trace=None, check_dispatch: bool = True,
                dedup: bool = False, capacity: int = 0, replan_interval: int = 1,
-               host_state: bool = False, lazy_replicate: bool = False):
+               host_state: bool = False, lazy_replicate: bool = False, seed: int | None = None):
     """Returns the number of iterations compared.  rank_mode: "virtual" (rank=-1, G ranks on
-    cuda:0) or "single" (real mode with G == 1)."""
+    cuda:0) or "single" (real mode with G == 1).  `name` is a config name or an ad-hoc
+    synth.configs.Workload (then pass `seed`)."""
     from paper_2504_19925_b200 import AdamConfig, DecoupledExpertLayer
     from paper_2504_19925_b200.api import synth_grads
     from oracle.adam import AdamHyper
 
-    wl = configs.CONFIGS[name]
+    wl = configs.CONFIGS[name] if isinstance(name, str) else name
     S = wl.S(G)
     E, k, P = wl.E, wl.k, wl.P
     TT = wl.T if T is None else T
     Tg = TT // G
-    seed = configs.seed_for(name)
+    if seed is None:
+        seed = configs.seed_for(name)
     rank = -1 if rank_mode == "virtual" else 0
     if rank == 0:
         assert G == 1
@@ -49,7 +51,7 @@ def run_parity(name: str, G: int, iters: int, *, rank_mode: str = "virtual", idx
     Pg = P // G
     # initial placement (moe_place) equals the oracle's plan_0 placement
     _compare_weights(layer, sim, idx_t, G, S, P)
-    tr = trace if trace is not None else traces.make_trace(wl, iters=iters, T=TT)
+    tr = trace if trace is not None else traces.make_trace(wl, iters=iters, T=TT, seed=seed)
     for t, (ids, gates) in enumerate(tr[:iters]):
         for v in range(layer.n_local):
             synth_grads(layer.slot_g[v], seed, t, v * S, S, P)

@@ -284,3 +284,26 @@ def test_repeated_expert_within_token_detected(k):
                 layer.ctx.check()
             assert ei.value.status == 3, (t, j0, j1)
     layer.close()
+
+
+@pytest.mark.parametrize("case", range(24))
+def test_random_small_configs_fuzz(case):
+    """Corner cases by construction: E from 1, k up to E, S down to ceil(E/G), G up to 8, T
+    down to 0 and ragged, P any multiple of 8G, random capacity / policy / interval / de-dup /
+    lazy replication -- every output of 2 iterations against the oracle."""
+    from gpu_helpers import run_parity
+    from oracle.dispatch import slot_capacity
+    rng = np.random.default_rng(1000 + case)
+    G = int(rng.choice([1, 2, 3, 4, 8]))
+    E = int(rng.integers(1, 25))
+    S = -(-E // G) + int(rng.integers(0, 5))
+    k = int(rng.integers(1, min(E, 4) + 1))
+    T = G * int(rng.integers(0, 300)) if case % 6 else 0
+    P = 8 * G * int(rng.integers(1, 40))
+    wl = configs.Workload(f"fuzz{case}", E=E, d=P, ffn=1, mats=1, k=k, T=T, slots_total=G * S,
+                          trace="walk-spike", G_default=G)
+    cap = slot_capacity(float(rng.uniform(0.3, 2.0)), T, k, G * S) if rng.random() < 0.4 else 0
+    dedup = G > 1 and rng.random() < 0.5
+    run_parity(wl, G, 2, T=T, seed=77 + case, policy=int(rng.integers(0, 3)),
+               replan_interval=int(rng.integers(1, 3)), capacity=cap, dedup=dedup,
+               lazy_replicate=dedup and rng.random() < 0.5)
