@@ -286,11 +286,12 @@ def test_repeated_expert_within_token_detected(k):
     layer.close()
 
 
-@pytest.mark.parametrize("case", range(24))
+@pytest.mark.parametrize("case", range(96))
 def test_random_small_configs_fuzz(case):
     """Corner cases by construction: E from 1, k up to E, S down to ceil(E/G), G up to 8, T
     down to 0 and ragged, P any multiple of 8G, random capacity / policy / interval / de-dup /
-    lazy replication -- every output of 2 iterations against the oracle."""
+    lazy replication / host-resident state / scale mode / weight decay -- every output of 2
+    iterations against the oracle."""
     from gpu_helpers import run_parity
     from oracle.dispatch import slot_capacity
     rng = np.random.default_rng(1000 + case)
@@ -304,6 +305,10 @@ def test_random_small_configs_fuzz(case):
                           trace="walk-spike", G_default=G)
     cap = slot_capacity(float(rng.uniform(0.3, 2.0)), T, k, G * S) if rng.random() < 0.4 else 0
     dedup = G > 1 and rng.random() < 0.5
+    scale_mode = int(rng.integers(0, 3))
+    scale = rng.uniform(0.25, 2.0, E).astype(np.float32) if scale_mode == 2 else None
     run_parity(wl, G, 2, T=T, seed=77 + case, policy=int(rng.integers(0, 3)),
                replan_interval=int(rng.integers(1, 3)), capacity=cap, dedup=dedup,
-               lazy_replicate=dedup and rng.random() < 0.5)
+               lazy_replicate=dedup and rng.random() < 0.5, host_state=rng.random() < 0.2,
+               scale_mode=scale_mode, scale=scale,
+               weight_decay=0.01 if rng.random() < 0.3 else 0.0)
