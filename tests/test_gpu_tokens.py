@@ -31,17 +31,20 @@ def _from_dev(t: torch.Tensor) -> np.ndarray:
     return t.view(torch.int16).cpu().numpy().view(np.uint16)
 
 
-def run_tokens(name: str, G: int, iters: int, cf: float = 0.0, flags: int = 0, T: int | None = None):
+def run_tokens(name, G: int, iters: int, cf: float = 0.0, flags: int = 0, T: int | None = None,
+               seed: int | None = None):
     from paper_2504_19925_b200 import DecoupledExpertLayer, TokenExchange, api
     from oracle import dispatch as OD
     from oracle import plan as OP
     from oracle import tokens as OT
-    wl = configs.CONFIGS[name]
+    wl = configs.CONFIGS[name] if isinstance(name, str) else name
+    if seed is None:
+        seed = configs.seed_for(wl.name)
     S, E, k, d = wl.S(G), wl.E, wl.k, wl.d
     TT = wl.T if T is None else T
     Tg = TT // G
     cap = OD.slot_capacity(cf, TT, k, G * S) if cf > 0 else 0
-    tr = traces.make_trace(wl, iters=iters, T=TT)
+    tr = traces.make_trace(wl, iters=iters, T=TT, seed=seed)
     # oracle routing for every iteration first (it sizes the buffers)
     plan = OP.plan(np.ones(E, np.int64), E, G, S)
     routes = []
@@ -52,7 +55,7 @@ def run_tokens(name: str, G: int, iters: int, cf: float = 0.0, flags: int = 0, T
     rows = max(1, max(int(dp["slot_load"].max()) for _, dp in routes))
     layer = DecoupledExpertLayer(E, G, S, k, 8 * G, Tg, rank=-1, device=0, seed=1, capacity=cap)
     tx = TokenExchange(layer.ctx, d, rows)
-    rng = np.random.default_rng(configs.seed_for(name) + 17)
+    rng = np.random.default_rng(seed + 17)
     use_gate = bool(flags & api.MOE_TOK_GATE)
     for it, ((ids, gates), (plan_t, disp)) in enumerate(zip(tr, routes)):
         layer.plan = api.Plan.from_first_slot(plan_t["first_slot"], G, S)
@@ -169,3 +172,21 @@ def test_context_close_closes_token_exchange_first():
     layer.close()                      # closes tx, then the context
     assert tx._h is None
     tx.close()                         # idempotent
+
+
+@pytest.mark.parametrize("case", range(40))
+def test_token_exchange_fuzz(case):
+    """Random E (from 1), G (to 8), S, k (to E), T (ragged, from 0), d (multiple of 8, also
+    not a multiple of the kernels' 128/256-vector chunks), capacity and gate flags."""
+    from oracle.dispatch import slot_capacity
+    rng = np.random.default_rng(5000 + case)
+    G = int(rng.choice([1, 2, 3, 4, 8]))
+    E = int(rng.integers(1, 20))
+    S = -(-E // G) + int(rng.integers(0, 4))
+    k = int(rng.integers(1, min(E, 5) + 1))
+    T = G * int(rng.integers(0, 200)) if case % 8 else 0
+    d = 8 * int(rng.integers(1, 160))
+    wl = configs.Workload(f"tfuzz{case}", E=E, d=d, ffn=1, mats=1, k=k, T=T, slots_total=G * S,
+                          trace="walk-spike", G_default=G)
+    cf = float(rng.uniform(0.3, 2.0)) if rng.random() < 0.4 else 0.0
+    run_tokens(wl, G, 2, cf=cf, flags=int(rng.integers(0, 2)), seed=900 + case)
