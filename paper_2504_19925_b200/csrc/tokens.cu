@@ -365,9 +365,11 @@ int alloc_base(const void *ptr, void **base) {
 int fill_args(moe_tokx *x, int64_t T, const float *gates, const moe_dispatch_out *out, int32_t flags,
               const char *what, TokArgs *a) {
   moe_ctx *c = x->ctx;
-  if (!out || !out->dest_slot || !out->dest_off) return fail(MOE_ERR_INVALID, "%s: NULL dispatch outputs", what);
   if (T < 0 || T > c->max_tokens) return fail(MOE_ERR_INVALID, "%s: T=%lld outside [0, max_tokens]", what, (long long)T);
-  if ((flags & MOE_TOK_GATE) && !gates) return fail(MOE_ERR_INVALID, "%s: MOE_TOK_GATE needs gates", what);
+  // like moe_dispatch, an empty iteration (T = 0) may pass NULL arrays
+  if (!out || (T > 0 && (!out->dest_slot || !out->dest_off)))
+    return fail(MOE_ERR_INVALID, "%s: NULL dispatch outputs", what);
+  if ((flags & MOE_TOK_GATE) && !gates && T > 0) return fail(MOE_ERR_INVALID, "%s: MOE_TOK_GATE needs gates", what);
   if (!x->connected) return fail(MOE_ERR_INVALID, "%s: call moe_tokx_connect first", what);
   memset(a, 0, sizeof(*a));
   for (int h = 0; h < c->G; ++h) {
