@@ -24,6 +24,7 @@ import torch.distributed as dist  # noqa: E402
 def main() -> int:
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="tiny-skew")
+    ap.add_argument("--adhoc", default=None, help="E,S_per_gpu,k,T,P,seed: an ad-hoc workload")
     ap.add_argument("--iters", type=int, default=6)
     ap.add_argument("--sampled", action="store_true", help="compare a sample of elements only")
     ap.add_argument("--trace", default="config", choices=["config", "rotating-hot"])
@@ -48,11 +49,16 @@ def main() -> int:
     from oracle import step as ostep
     from synth import configs, hashgen, traces
 
-    wl = configs.CONFIGS[args.config]
+    if args.adhoc:
+        aE, aS, ak, aT, aP, aseed = (int(x) for x in args.adhoc.split(","))
+        wl = configs.Workload(f"adhoc{aseed}", E=aE, d=aP, ffn=1, mats=1, k=ak, T=aT, slots_total=aS * G,
+                              trace="walk-spike", G_default=G)
+    else:
+        wl = configs.CONFIGS[args.config]
     S, E, k, P = wl.S(G), wl.E, wl.k, wl.P
     Tg = wl.tokens_per_rank(G)
     Pg = P // G
-    seed = configs.seed_for(wl.name)
+    seed = aseed if args.adhoc else configs.seed_for(wl.name)
     from oracle.dispatch import slot_capacity
     cap = slot_capacity(args.cf, wl.T, k, G * S) if args.cf > 0 else 0
     layer = DecoupledExpertLayer(E, G, S, k, P, Tg, rank=rank, device=local, seed=seed,
@@ -67,7 +73,7 @@ def main() -> int:
         from oracle import plan as OP
         from oracle import tokens as OT
         from oracle.numerics import f32_to_bf16_rne
-        trc = traces.make_trace(wl, iters=args.iters) if args.trace == "config" else \
+        trc = traces.make_trace(wl, iters=args.iters, seed=seed) if args.trace == "config" else \
             traces.rotating_hot(E, wl.T, k, args.iters, seed=seed, hot_weight=4 if E < 16 else 16)
         pl = OP.plan(np.ones(E, np.int64), E, G, S, {0: "alg1", 1: "minmax", 2: "static"}[args.policy])
         rows = 1
@@ -97,7 +103,7 @@ def main() -> int:
     if args.trace == "rotating-hot":
         tr = traces.rotating_hot(E, wl.T, k, args.iters, seed=seed, hot_weight=4 if E < 16 else 16)
     else:
-        tr = traces.make_trace(wl, iters=args.iters)
+        tr = traces.make_trace(wl, iters=args.iters, seed=seed)
     ok = True
     msgs = []
 

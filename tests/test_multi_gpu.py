@@ -39,6 +39,11 @@ def _torchrun(n: int, *args, timeout=600):
     (4, "tiny-skew", ["--tokens", "1", "--dedup", "--trace", "rotating-hot"]),
     (4, "medium", ["--host-state", "--dedup", "--iters", "4"]), (2, "medium", ["--host-state", "--iters", "3"]),
     (4, "medium", ["--dedup", "--lazy", "--iters", "4"]), (2, "tiny-skew", ["--dedup", "--lazy", "--tokens", "1"]),
+    # ad-hoc random shapes (E, S per GPU, k, T, P, seed): ragged owner ranges, k = E, E = 1
+    (2, "tiny", ["--adhoc", "7,5,3,602,528,11", "--dedup", "--lazy", "--cf", "0.8", "--tokens", "1"]),
+    (4, "tiny", ["--adhoc", "13,4,2,1000,1344,12", "--dedup", "--tokens", "0"]),
+    (4, "tiny", ["--adhoc", "3,3,3,404,96,13", "--policy", "1", "--interval", "2", "--iters", "5"]),
+    (2, "tiny", ["--adhoc", "1,2,1,300,208,14", "--host-state"]),
 ], ids=lambda x: "".join(a.lstrip("-") for a in x) if isinstance(x, list) else str(x))
 def test_real_multi_gpu_parity(G, config, extra):
     if torch.cuda.device_count() < G:
