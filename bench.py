@@ -455,13 +455,14 @@ def gpu_arm(args, wl):
     updk_avg_local = tm["update_kernel_ms"] / max(1, tm["n_update_kernel"])
     host_wait_local = tm["host_wait_ms"] / K
     host_plan_local = tm["host_plan_ms"] / K
+    host_launch_local = tm["host_launch_ms"] / K
     if args.host_state:   # row f4: one step = several windowed launches + copies; time the stage
         updk_avg_local = upd_avg_local
     t = torch.tensor([total_ms, upd_avg_local, disp_avg_local, pre_avg_local, rep_avg_local,
-                      updk_avg_local, host_wait_local, host_plan_local], device="cuda")
+                      updk_avg_local, host_wait_local, host_plan_local, host_launch_local], device="cuda")
     if G > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms, upd_avg, disp_avg, pre_avg, rep_avg, updk_avg, hw_avg, hp_avg = (float(x) for x in t.tolist())
+    total_ms, upd_avg, disp_avg, pre_avg, rep_avg, updk_avg, hw_avg, hp_avg, hl_avg = (float(x) for x in t.tolist())
     # per-iteration step times, max over ranks (SURVEY d.4: median, p10, p90)
     per_step = torch.tensor([step_ev[i].elapsed_time(step_ev[i + 1]) for i in range(K)], device="cuda")
     if G > 1:
@@ -612,6 +613,7 @@ def gpu_arm(args, wl):
                           "presum": round(pre_avg, 4), "replicate": round(rep_avg, 4),
                           "host_enqueue_per_step": round(host_ms, 4),
                           "host_wait_counts": round(hw_avg, 4), "host_planner": round(hp_avg, 4),
+                          "host_update_launch": round(hl_avg, 4),
                           "note": "library CUDA events (moe_ctx_set_timing) on the launching stream: "
                                   "the 3 dispatch kernels; the update stage (= k_update_tma, or with "
                                   "de-dup k_presum + k_update_tma + k_replicate); max over ranks"},

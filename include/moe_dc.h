@@ -50,7 +50,7 @@
 extern "C" {
 #endif
 
-#define MOE_ABI_VERSION 4
+#define MOE_ABI_VERSION 5
 #define MOE_MAX_E 256     /* experts per layer                              */
 #define MOE_MAX_G 8       /* GPUs: one NVSwitch box                         */
 #define MOE_MAX_SLOTS 4096 /* G*S                                           */
@@ -195,8 +195,8 @@ int moe_ctx_get_timing(moe_ctx *ctx, double *dispatch_ms, int64_t *n_dispatch, d
  * MOE_T_REPLICATE (de-dup kernels), MOE_T_STAGE (the whole update stage: presum + update +
  * replicate; equals MOE_T_UPDATE without de-dup).  moe_ctx_get_timing's update_ms is
  * MOE_T_STAGE.  Host stages of moe_step (wall clock, recorded while timing is enabled):
- * MOE_T_HOST_WAIT (waiting for C_t to reach pinned host memory) and MOE_T_HOST_PLAN (the
- * planner: Alg. 1 or the policy's copy).                                                   */
+ * MOE_T_HOST_WAIT (waiting for C_t to reach pinned host memory), MOE_T_HOST_PLAN (the
+ * planner: Alg. 1 or the policy's copy) and MOE_T_HOST_LAUNCH (enqueueing the update).     */
 #define MOE_T_DISPATCH 0
 #define MOE_T_UPDATE 1
 #define MOE_T_PRESUM 2
@@ -204,7 +204,8 @@ int moe_ctx_get_timing(moe_ctx *ctx, double *dispatch_ms, int64_t *n_dispatch, d
 #define MOE_T_STAGE 4
 #define MOE_T_HOST_WAIT 5
 #define MOE_T_HOST_PLAN 6
-#define MOE_TIMING_STAGES 7
+#define MOE_T_HOST_LAUNCH 7
+#define MOE_TIMING_STAGES 8
 int moe_ctx_get_timing_ex(moe_ctx *ctx, double *ms, int64_t *n);
 
 /* Synchronises `stream`, then reports and clears device-raised errors

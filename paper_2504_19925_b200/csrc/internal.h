@@ -120,8 +120,8 @@ struct moe_ctx {
 
   // measurement hooks (moe_ctx_set_timing): event pairs per stage, recycled
   bool timing;
-  double host_ms[2];    // MOE_T_HOST_WAIT, MOE_T_HOST_PLAN (moe_step, wall clock)
-  int64_t host_n[2];
+  double host_ms[3];    // MOE_T_HOST_WAIT, _PLAN, _LAUNCH (moe_step, wall clock)
+  int64_t host_n[3];
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool, ev_disp, ev_upd, ev_presum, ev_repl, ev_stage;
 };
 

@@ -45,7 +45,10 @@ extern "C" int moe_step(moe_ctx *ctx, const int32_t *topk_ids, const float *gate
                      nullptr);  // a1 -> plan_{t+1}
     if (st) return moe_step_abort(ctx, st);
   }
+  const auto t2 = clk::now();
+  st = moe_update(ctx, plan_cur, plan_next, adam, stream);  // a3 + a4 + a5
   moe_host_time(ctx, 0, std::chrono::duration<double, std::milli>(t1 - t0).count());
-  moe_host_time(ctx, 1, std::chrono::duration<double, std::milli>(clk::now() - t1).count());
-  return moe_update(ctx, plan_cur, plan_next, adam, stream);  // a3 + a4 + a5
+  moe_host_time(ctx, 1, std::chrono::duration<double, std::milli>(t2 - t1).count());
+  moe_host_time(ctx, 2, std::chrono::duration<double, std::milli>(clk::now() - t2).count());
+  return st;
 }

@@ -37,7 +37,7 @@ def test_exports_every_declared_symbol(lib):
     assert declared == set(_lib.EXPORTED)
     for name in declared:
         assert hasattr(lib, name), name
-    assert lib.moe_abi_version() == 4
+    assert lib.moe_abi_version() == 5
     assert lib.moe_status_str(3) == b"MOE_ERR_DATA"
     assert lib.moe_ctx_handle_bytes() >= 3 * 64
 
