@@ -19,11 +19,16 @@ def _free_port() -> int:
     return p
 
 
-def _torchrun(n: int, *args, timeout=600):
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
-           os.path.join(ROOT, "tests", "mp_parity.py"), *args]
-    return subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
+def _torchrun(n: int, *args, timeout=600, script="mp_parity.py"):
+    """torchrun on a free port; retried with a new port if the rendezvous lost a port race."""
+    for _ in range(3):
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+               "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+               os.path.join(ROOT, "tests", script), *args]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
+        if r.returncode == 0 or "EADDRINUSE" not in (r.stdout + r.stderr):
+            return r
+    return r
 
 
 @pytest.mark.parametrize("G,config,extra", [
@@ -57,8 +62,5 @@ def test_missing_peer_times_out_instead_of_hanging():
     """Failure detection: a rank that skips an iteration -> MOE_ERR_TIMEOUT on its peer (~30 s)."""
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
-           os.path.join(ROOT, "tests", "mp_failure.py")]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
+    r = _torchrun(2, timeout=300, script="mp_failure.py")
     assert r.returncode == 0 and "mp_failure: OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
