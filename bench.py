@@ -292,7 +292,8 @@ def token_a2a(args, wl, layer, gates, G, rank, Tg, S, peak_hbm, barrier, stream)
     routing of the last timed iteration: bf16 activations [T_g][d] -> expert buffers ->
     [T_g][d].  Algorithmic bytes per GPU: HBM = (T_g + rows landing in this
     GPU's slots) * d * 2 per kernel; NVLink per direction = max(pairs this GPU sends to / pulls
-    from other GPUs, pairs other GPUs send to / pull from it) * d * 2."""
+    from other GPUs, pairs other GPUs send to / pull from it) * d * 2; the roofline takes the
+    busiest GPU (max over ranks)."""
     import torch
     import torch.distributed as dist
     from paper_2504_19925_b200 import TokenExchange, api
@@ -342,6 +343,10 @@ def token_a2a(args, wl, layer, gates, G, rank, Tg, S, peak_hbm, barrier, stream)
     disp_ms, comb_ms = (float(x) for x in t.tolist())
     hbm = (Tg + rows_in) * d * 2
     nvl = max(remote_out, remote_in) * d * 2
+    if G > 1:  # the busiest GPU bounds the exchange (a hot slot's GPU receives far more rows)
+        b = torch.tensor([hbm, nvl], dtype=torch.float64, device="cuda")
+        dist.all_reduce(b, op=dist.ReduceOp.MAX)
+        hbm, nvl = int(b[0].item()), int(b[1].item())
     tx.close()
 
     def roof(ms):
@@ -359,7 +364,7 @@ def token_a2a(args, wl, layer, gates, G, rank, Tg, S, peak_hbm, barrier, stream)
             "hbm_bytes_per_kernel": hbm, "nvlink_bytes_per_kernel_per_dir": nvl,
             "dispatch_roofline": roof(disp_ms), "combine_roofline": roof(comb_ms),
             "note": "row f3 forward pair (copy dispatch, gate-weighted combine) on the last timed iteration's routing; "
-                    "rank 0's bytes, max-over-ranks times; not part of `value`"}
+                    "bytes of the busiest GPU, max-over-ranks times; not part of `value`"}
 
 
 # ------------------------------------------------------------------------------------------
