@@ -10,7 +10,9 @@ op for the reduce and Adam, exactly as the paper's / DESIGN.md's op order).
 Every function cites the passage it follows:
 
   plan.py      Alg. 1 (apx:algo_scheduler) + MINMAX reading A1
-  dispatch.py  step 2 replica load-balancing + A8
+               + the static baseline (row f2, reading B2)
+  dispatch.py  step 2 replica load-balancing (PAPER.md:690-692, 893-898) + A8;
+               capacity/drops and the policy drop study (row f2, B1/B3)
   reduce.py    intra+inter-rank all-reduce order and normalisation
                (PAPER.md:965-969, sec:comm_allreduce) + A10, A11
   adam.py      optimizer step 5 + A15 op order
@@ -18,9 +20,12 @@ Every function cites the passage it follows:
   place.py     step 8 new-placement materialisation
   step.py      one iteration over G simulated ranks + the App. E byte count
                (PAPER.md:1600-1625, apx:nonoffload)
+  tokens.py    the token all-to-all along the routing (row f3; C1-C3)
 
 Pins (tests/test_oracle_*.py, ``-m "not gpu"``): SPEC worked examples, exact
 apportionment characterisations, brute-force exhaustive search, stable argsort,
 closed forms for Adam, torch.optim.Adam within 1e-6, torch's bf16 rounding,
-the App. E closed-form volume.  No function here is "parity unpinned".
+the App. E closed-form volume, the step composition (A7), token round trips and the
+adjoint identity, the policy drop ordering; a mutation sweep checks that
+plausible one-line mistakes fail a pin.  No function here is "parity unpinned".
 """
