@@ -22,6 +22,12 @@
  *                      updated bf16 shards are written straight into the slots
  *                      of the NEXT placement (no separate migration). -> moe_update
  *
+ * Beyond the five stages, all opt-in and bit-identical where they apply:
+ *   f1 MOE_OPT_DEDUP (+ MOE_OPT_LAZY_REPLICATE)  locality de-duplication of the NVLink traffic
+ *   f2 moe_dispatch_out.capacity / .drops, moe_slot_capacity, MOE_PLAN_STATIC / MOE_PLAN_KEEP
+ *   f3 include/moe_tokens.h                      token all-to-all along the dispatch's routing
+ *   f4 MOE_OPT_HOST_STATE                        optimizer shards in pinned host DRAM
+ *
  * Conventions (every function):
  *   - Returns an int status (moe_status); 0 == MOE_OK.  No C++ exception ever
  *     crosses this boundary.  On failure moe_last_error() gives a thread-local
