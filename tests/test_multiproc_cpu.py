@@ -44,6 +44,21 @@ def _worker(rank, world, port, q):
         c = torch.from_numpy(od.counts([mine], wl.E)[0])
         dist.all_reduce(c)
         ok &= c.tolist() == np.bincount(ids.reshape(-1), minlength=wl.E).tolist()
+        # every rank plans plan_{t+1} itself (host C++, no GPU): the plans must be identical
+        from paper_2504_19925_b200 import api, _lib
+        S = wl.S(world)
+        plan = api.moe_plan(c.numpy().astype(np.int64), wl.E, world, S)
+        allp = [None] * world
+        dist.all_gather_object(allp, (plan.replicas.tolist(), plan.first_slot.tolist()))
+        ok &= all(p == allp[0] for p in allp)
+        from oracle import plan as op
+        ok &= allp[0][0] == op.alg1(c.numpy(), wl.E, world, S).tolist()
+        # record exchange at the library's real record sizes (context and token exchange)
+        L = _lib.lib()
+        for nbytes in (L.moe_ctx_handle_bytes(), L.moe_tokx_handle_bytes()):
+            rec = bytes([(rank * 7 + i) % 256 for i in range(nbytes)])
+            recs = gather_records(rec, world)
+            ok &= recs == [bytes([(r * 7 + i) % 256 for i in range(nbytes)]) for r in range(world)]
         q.put((rank, bool(ok)))
     finally:
         dist.destroy_process_group()
