@@ -74,3 +74,24 @@ def test_drop_ordering_per_iteration_interval_static(seed):
     assert rate["per"] < rate["i10"] <= rate["i50"] + 1 and rate["i50"] <= rate["i100"] + 1
     assert rate["i100"] < rate["static"]
     assert rate["static"] - rate["per"] >= 10, rate
+
+
+@pytest.mark.parametrize("policy,interval", [("alg1", 1), ("alg1", 3), ("static", 1), ("minmax", 2)])
+def test_pair_level_sim_and_count_level_policy_agree(policy, interval):
+    """Reading B3's schedule, pinned both ways: OracleSim (pair-level dispatch with capacity,
+    re-planning when its step counter hits a multiple of the interval) and policy_drops
+    (count-level, re-planning after iterations t with (t+1) % i == 0) give the same drops."""
+    from oracle import step as ST
+    from synth import hashgen
+    E, G, S, T, k, P = 8, 2, 6, 512, 2, 64
+    cap = OD.slot_capacity(0.8, T, k, G * S)
+    tr = traces.walk_spike(E, T, k, 9, seed=21)
+    sim = ST.OracleSim(E, G, S, P, 5, policy=policy, capacity=cap, replan_interval=interval,
+                       idx=np.arange(8, dtype=np.int64))
+    got = []
+    for t, (ids, gates) in enumerate(tr):
+        res = sim.iterate(traces.split_ranks(ids, G), traces.split_ranks(gates, G),
+                          lambda j, t=t: hashgen.grad_bits(5, t, j, np.arange(8, dtype=np.uint64)))
+        got.append(int(res["dispatch"]["drops"].sum()))
+    want = OD.policy_drops([traces.expert_counts(i, E) for i, _ in tr], E, G, S, cap, policy, interval)
+    assert got == want["drops"].tolist()
