@@ -160,9 +160,11 @@ typedef struct {
 /* Row f4 (host-offloaded optimizer shards; PAPER.md:705, 734-736, 839-841 -- the paper's
  * deployed design keeps the fp32 optimizer state in host DRAM): master/adam_m/adam_v are
  * PINNED HOST memory (cudaHostAlloc / cudaHostRegister; with unified addressing the host
- * pointer is device-accessible).  The same fused update kernel then streams the 12 B/param
- * of state in and out over PCIe (zero-copy) while grads and weights stay in HBM; results are
- * bit-identical.  moe_ctx_create fails with MOE_ERR_INVALID if the pointers are not pinned
+ * pointer is device-accessible).  moe_update then streams the 12 B/param of state through a
+ * 3-deep HBM staging ring (~64 MB windows of every expert): copy-engine H2D of window i+1,
+ * the same fused kernel on window i, D2H of window i-1, overlapped; grads and weights stay in
+ * HBM and results are bit-identical.  The library allocates the staging ring (192 MB) and two
+ * copy streams.  moe_ctx_create fails with MOE_ERR_INVALID if the pointers are not pinned
  * host memory (or, without the option, if they are not device memory).                */
 #define MOE_OPT_HOST_STATE 2
 
@@ -176,17 +178,26 @@ typedef struct {
 
 /* Creates a context (allocates scratch and the sync buffer on desc->device).
  * Virtual mode is ready immediately.  Real mode (G > 1) additionally needs
- * moe_ctx_export + an exchange of the handles between ranks + moe_ctx_connect.  */
+ * moe_ctx_export + an exchange of the handles between ranks + moe_ctx_connect.
+ * The caller's buffers must outlive the context; the context must outlive every token
+ * exchange bound to it (moe_tokens.h).
+ * Errors: MOE_ERR_INVALID -- E, G, S, k < 1, E > G*S, k > E, limits (MOE_MAX_*), P % G != 0
+ * or (P/G) % 8 != 0, max_tokens*k*G >= 2^31, rank outside [-1, G), a NULL or not 16-byte
+ * aligned buffer, state memory not matching MOE_OPT_HOST_STATE; MOE_ERR_CUDA -- an
+ * allocation or stream/event creation failed (nothing is leaked).                        */
 int moe_ctx_create(const moe_ctx_desc *desc, moe_ctx **out);
 int moe_ctx_destroy(moe_ctx *ctx);
 
 /* Bytes of this rank's peer-mapping record (CUDA IPC handles + offsets).        */
 int moe_ctx_handle_bytes(void);
-/* Writes this rank's record into out[moe_ctx_handle_bytes()] (host).            */
+/* Writes this rank's record into out[moe_ctx_handle_bytes()] (host).
+ * Errors: MOE_ERR_INVALID (virtual-mode context), MOE_ERR_COMM / MOE_ERR_CUDA (IPC).      */
 int moe_ctx_export(moe_ctx *ctx, void *out);
 /* all: G records in rank order (host), as gathered by the caller's process group.
- * Maps every peer's slot_g / slot_w / sync buffer.  Collective in spirit: every rank
- * must connect before any rank's first moe_dispatch / moe_update.               */
+ * Maps every peer's slot_g / slot_w / sync buffer (and de-dup partials).  Collective in
+ * spirit: every rank must connect before any rank's first moe_dispatch / moe_update.
+ * Errors: MOE_ERR_INVALID (virtual mode; ranks disagree on MOE_OPT_DEDUP), MOE_ERR_COMM
+ * (cudaIpcOpenMemHandle failed).                                                        */
 int moe_ctx_connect(moe_ctx *ctx, const void *all);
 
 /* Measurement hooks.  While enabled, the library records CUDA events on the launching stream
