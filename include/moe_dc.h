@@ -229,10 +229,12 @@ int moe_ctx_get_timing_ex(moe_ctx *ctx, double *ms, int64_t *n);
  * (MOE_ERR_DATA, MOE_ERR_TIMEOUT).                                               */
 int moe_ctx_check(moe_ctx *ctx, void *stream);
 
-/* Blocks the calling host thread until the C_e copy of the most recent moe_dispatch
- * has landed in out->counts_host (an event recorded right after that copy, BEFORE the
- * scatter kernel), so the host planner (step 6 may "execute earlier, even right after
- * step 1", PAPER.md:709 fn) overlaps the scatter.  MOE_OK if no dispatch was issued.  */
+/* Blocks the calling host thread until the C_e of the most recent moe_dispatch have landed
+ * in out->counts_host: the scan kernel's last block writes them to the pinned buffer and
+ * releases a pinned host flag (system scope) that this call spins on -- BEFORE the scatter
+ * kernel, so the host planner (step 6 may "execute earlier, even right after step 1",
+ * PAPER.md:709 fn) overlaps the scatter.  MOE_OK if no dispatch was issued;
+ * MOE_ERR_TIMEOUT after 30 s (e.g. a peer never arrived), MOE_ERR_CUDA on a sticky error. */
 int moe_ctx_wait_counts(moe_ctx *ctx);
 
 /* Makes `stream` wait until every slot weight of the last moe_update / moe_place is in place
@@ -269,6 +271,11 @@ typedef struct {
   int64_t *drops;       /* [E] dropped pairs per expert (device, nullable)                  */
 } moe_dispatch_out;
 
+/* Errors (returned): MOE_ERR_INVALID -- T < 0 or T > max_tokens, a NULL buffer (the
+ * per-pair arrays may be NULL when T == 0), capacity < 0, a real-mode context not connected,
+ * counts_host not pinned; MOE_ERR_SHAPE -- plan not a valid placement for the context.
+ * Device-raised (reported by moe_ctx_check): MOE_ERR_DATA -- an id outside [0, E) or repeated
+ * within a token (outputs undefined); MOE_ERR_TIMEOUT -- a peer's counts never arrived.    */
 int moe_dispatch(moe_ctx *ctx, const int32_t *topk_ids, const float *gates, int64_t T,
                  const moe_plan_t *plan, const moe_dispatch_out *out, void *stream);
 
@@ -289,6 +296,12 @@ typedef struct {
   const float *scale;   /* [E] host, mode 2 only                                      */
 } moe_adam_t;
 
+/* Reads the slot grads (plan_cur's slots), updates the owner shards in place, writes the slot
+ * weights of plan_next (every GPU's, through the peer mappings).
+ * Errors (returned): MOE_ERR_INVALID -- NULL ctx/adam, step < 1, bad scale_mode / scale, a
+ * real-mode context not connected; MOE_ERR_SHAPE -- a plan not valid for the context;
+ * MOE_ERR_CUDA.  Device-raised (moe_ctx_check): MOE_ERR_TIMEOUT -- a peer never reached a
+ * barrier.                                                                                */
 int moe_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *plan_next,
                const moe_adam_t *adam, void *stream);
 
@@ -303,6 +316,10 @@ int moe_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *plan_
  *                                                             step 1", PAPER.md:709 fn)
  *   moe_update(plan_cur, plan_next, adam)                    a3+a4+a5  (device, async)
  * plan_next: caller-allocated arrays, filled here.  Returns after the update is enqueued.
+ * Scheduling inside: with MOE_OPT_DEDUP the local partial sums start first on a library side
+ * stream; the three dispatch kernels run on a highest-priority library stream; both are
+ * joined to `stream` by events, so the caller sees ordinary stream semantics.
+ * policy: a moe_plan_policy (MOE_PLAN_KEEP = keep plan_cur, the interval policy).
  * Errors: those of the four calls; MOE_ERR_INVALID if out->counts_host is NULL.           */
 int moe_step(moe_ctx *ctx, const int32_t *topk_ids, const float *gates, int64_t T,
              const moe_plan_t *plan_cur, moe_plan_t *plan_next, int32_t policy,
