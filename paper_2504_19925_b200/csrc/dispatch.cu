@@ -40,6 +40,10 @@ struct HistArgs {
   uint32_t *done;      // [n_local]
   int32_t *err;
   SyncBuf *dst[MOE_MAX_G];  // real: every GPU's sync buffer; virtual: dst[0] = the shared one
+  // one GPU (G == 1): the last tile already holds C_e -- it publishes them to the host
+  // (pinned counts_host + the host flag) so the planner starts before k_scan runs
+  int64_t *counts_host;     // device alias of the pinned buffer, or nullptr
+  uint32_t *host_flag;
 };
 
 __global__ void __launch_bounds__(kThreads) k_hist(const __grid_constant__ HistArgs a) {
@@ -107,12 +111,16 @@ __global__ void __launch_bounds__(kThreads) k_hist(const __grid_constant__ HistA
   // peers (real mode, G > 1) acquire the counts through a system-scope flag; on one GPU the
   // dependent k_scan's griddepcontrol.wait already orders them
   const bool flags = a.real && a.G > 1;
-  if (flags) __threadfence_system();
+  const bool host = a.G == 1 && a.counts_host != nullptr;  // C_e = this rank's counts
+  if (host)
+    for (int e = tid; e < a.E; e += kThreads) a.counts_host[e] = a.dst[0]->xcnt[a.parity][grank][e];
+  if (flags || host) __threadfence_system();
   __syncthreads();
   if (tid == 0) {
     a.done[v] = 0;
     if (flags)
       for (int h = 0; h < a.G; ++h) st_release_sys(&a.dst[h]->disp_flag[grank], a.epoch);
+    if (host) st_release_sys(a.host_flag, a.epoch);
   }
 }
 
@@ -273,13 +281,16 @@ __global__ void __launch_bounds__(kThreads) k_scan(const __grid_constant__ ScanA
   __syncthreads();
   if (s_last) {
     __threadfence();
-    if (a.counts_host)
+    const bool publish = a.G > 1 || !a.counts_host;  // on one GPU k_hist already did
+    if (publish && a.counts_host)
       for (int x = tid; x < a.E; x += kThreads) a.counts_host[x] = __ldcg(a.counts_dev + x);
     __syncthreads();
     if (tid == 0) {
       *a.scan_done = 0;
-      __threadfence_system();
-      st_release_sys(a.host_flag, a.epoch);
+      if (publish) {
+        __threadfence_system();
+        st_release_sys(a.host_flag, a.epoch);
+      }
     }
   }
 }
@@ -511,6 +522,17 @@ extern "C" int moe_dispatch(moe_ctx *ctx, const int32_t *topk_ids, const float *
   ha.done = ctx->done;
   ha.err = ctx->err;
   for (int h = 0; h < MOE_MAX_G; ++h) ha.dst[h] = real ? ctx->peer_sync[h] : ctx->sync;
+  int64_t *counts_host_dev = nullptr;
+  if (out->counts_host) {  // C_t goes straight to pinned host memory (PAPER.md:709 fn: plan early)
+    void *dptr = nullptr;
+    if (cudaHostGetDevicePointer(&dptr, out->counts_host, 0) != cudaSuccess || !dptr) {
+      cudaGetLastError();
+      return fail(MOE_ERR_INVALID, "moe_dispatch: counts_host must be pinned (page-locked) host memory");
+    }
+    counts_host_dev = (int64_t *)dptr;
+  }
+  ha.counts_host = counts_host_dev;
+  ha.host_flag = ctx->host_flag_dev;
   const auto tev = timing_begin(ctx, s);
   k_hist<<<nb * ctx->n_local, kThreads, 0, s>>>(ha);
   MOE_CUDA_TRY(cudaGetLastError());
@@ -531,15 +553,7 @@ extern "C" int moe_dispatch(moe_ctx *ctx, const int32_t *topk_ids, const float *
   sa.slot_load = out->slot_load;
   sa.send_count = out->send_count;
   sa.counts_dev = out->counts_dev ? out->counts_dev : ctx->counts_dev;
-  sa.counts_host = nullptr;
-  if (out->counts_host) {  // C_t goes straight to pinned host memory (PAPER.md:709 fn: plan early)
-    void *dptr = nullptr;
-    if (cudaHostGetDevicePointer(&dptr, out->counts_host, 0) != cudaSuccess || !dptr) {
-      cudaGetLastError();
-      return fail(MOE_ERR_INVALID, "moe_dispatch: counts_host must be pinned (page-locked) host memory");
-    }
-    sa.counts_host = (int64_t *)dptr;
-  }
+  sa.counts_host = counts_host_dev;
   sa.scan_done = ctx->scan_done;
   sa.host_flag = ctx->host_flag_dev;
   sa.err = ctx->err;
