@@ -6,12 +6,15 @@ One step = one pass of the whole hot path over one iteration 
 synthetic routing trace: a0 count exchange + a2 dispatch (device) -> a1 Alg. 1 plan for t+1
 (host C++, overlapping the scatter) -> a3 reduce + a4 Adam + a5 place (one fused kernel).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config gpt-small] [--impl reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config qwen3-fine] [--impl reference]
 
-N = 1: the GPT-MoE-small workload (BASELINE.json configs[1]) with all 64 slots on one GPU.
-N > 1 (torchrun, one process per GPU): the same workload, S*G = 64 fixed (strong scaling);
-real mode with CUDA-IPC peer mappings over NVLink.  Timing: W warm-up steps, then exactly K
-steps between barrier + synchronize, CUDA events on the launching stream, max over ranks.
+Default workload: Qwen3-MoE-like fine-grained (BASELINE.json configs[3]: E 128, d 2048,
+ffn 768 SwiGLU, top-8, 524 288 tokens; 604 M expert parameters, 19.4 GB moved per step at
+N = 1) -- the largest configuration that fits one GPU (Mixtral-like needs ~225 GB).  N = 1
+holds all 256 slots; N > 1 (torchrun, one process per GPU) the same workload with S*G = 256
+fixed (strong scaling), real mode with CUDA-IPC peer mappings over NVLink.  Timing: W
+warm-up steps, then exactly K steps between barrier + synchronize, CUDA events on the
+launching stream, max over ranks.  `--config gpt-small` etc. select the other workloads.
 """
 from __future__ import annotations
 
@@ -148,23 +151,112 @@ def update_stage_bytes(fs_cur, fs_next, G: int, S: int, P: int, E: int, dedup: b
 
 
 # ------------------------------------------------------------------------------------------
-# reference arm / cpu_baseline: the oracle as it stands, on a bounded sample
+# reference arm / cpu_baseline: the oracle as it stands, on the FULL workload
 # ------------------------------------------------------------------------------------------
-def run_oracle_sample(wl, G: int, iters: int, frac_den: int = 256, seed_shift: int = 0):
-    """Times OracleSim on the SAME workload: full count exchange + dispatch + plan for all
-    T*k pairs, and reduce/Adam/place on 1/frac_den of every expert's elements (stride
-    sample), extrapolated x frac_den (every stage after dispatch is elementwise per expert).
-    Returns (ms per full iteration, description, per-iteration seconds)."""
+_ORACLE_TRACE = None   # set before the workers fork (inherited copy-on-write)
+
+
+def _oracle_worker(conn, wl_name: str, G: int, lo: int, hi: int, seed: int, core):
+    """One element range [lo, hi) of every expert: OracleSim (oracle/step.py, unchanged) with
+    idx = that range -- every stage after the dispatch is elementwise per expert, so the
+    workers together compute exactly the full iteration; each also runs the full a0/a2
+    dispatch and a1 plan (they need plan_{t+1})."""
+    from oracle import step as ostep
+    from synth import configs, hashgen, traces
+    if core is not None:
+        os.sched_setaffinity(0, {core})
+    wl = configs.CONFIGS[wl_name]
+    idx = np.arange(lo, hi, dtype=np.int64)
+    sim = ostep.OracleSim(wl.E, G, wl.S(G), wl.P, seed, idx=idx)
+    iu = idx.astype(np.uint64)
+    # the GPU arm's grads: api.synth_grads(t = 0) once, the same every step
+    grads = {j: hashgen.grad_bits(seed, 0, j, iu) for j in range(G * wl.S(G))}
+    conn.send("ready")
+    while True:
+        i = conn.recv()
+        if i is None:
+            break
+        ids, gates = _ORACLE_TRACE[i % len(_ORACLE_TRACE)]
+        t0 = time.perf_counter()
+        sim.iterate(traces.split_ranks(ids, G), traces.split_ranks(gates, G), grads.__getitem__)
+        conn.send((time.perf_counter() - t0, sim.stage_s))
+    conn.close()
+
+
+def run_oracle_full(wl, G: int, warmup: int, iters: int, n_tr: int, workers: int | None = None):
+    """Times oracle.step.OracleSim over the FULL workload (every pair, every element of every
+    expert, no extrapolation): the element range is split over `workers` processes, one host
+    core each, stepped in lock-step; the iteration's wall time runs from the step message to
+    the last worker's reply.  Same trace (n_tr iterations, cycled), seed and grads as the GPU
+    arm.  Returns a dict with the timed per-iteration seconds and per-stage medians."""
+    global _ORACLE_TRACE
+    import multiprocessing as mp
+    from synth import configs, traces
     os.environ.setdefault("OMP_NUM_THREADS", "1")
-    # SURVEY d.5: one host core (pinned for the timing, restored after)
-    prev_aff = os.sched_getaffinity(0) if hasattr(os, "sched_getaffinity") else None
-    if prev_aff:
-        os.sched_setaffinity(0, {min(prev_aff)})
+    cores = sorted(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else list(range(os.cpu_count() or 1))
+    C = max(1, min(workers or len(cores), len(cores), 64))
+    seed = configs.seed_for(wl.name)
+    t_setup = time.perf_counter()
+    _ORACLE_TRACE = traces.make_trace(wl, iters=n_tr, workers=C)
+    ctx = mp.get_context("fork")
+    P = wl.P
+    bounds = [P * c // C for c in range(C + 1)]
+    procs, conns = [], []
+    for c in range(C):
+        a, b = ctx.Pipe()
+        pr = ctx.Process(target=_oracle_worker, args=(b, wl.name, G, bounds[c], bounds[c + 1], seed,
+                                                      cores[c] if C <= len(cores) else None), daemon=True)
+        pr.start()
+        procs.append(pr)
+        conns.append(a)
+    for cn in conns:
+        assert cn.recv() == "ready"
+    setup_s = time.perf_counter() - t_setup
+    walls, stages = [], []
     try:
-        return _run_oracle_sample(wl, G, iters, frac_den, seed_shift)
+        for i in range(warmup + iters):
+            t0 = time.perf_counter()
+            for cn in conns:
+                cn.send(i)
+            rep = [cn.recv() for cn in conns]
+            w = time.perf_counter() - t0
+            if i >= warmup:
+                walls.append(w)
+                stages.append({k: max(r[1][k] for r in rep) for k in rep[0][1]})
     finally:
-        if prev_aff:
-            os.sched_setaffinity(0, prev_aff)
+        for cn in conns:
+            try:
+                cn.send(None)
+            except Exception:
+                pass
+        for pr in procs:
+            pr.join(timeout=30)
+        _ORACLE_TRACE = None
+    st = {k: round(1000.0 * statistics.median(s_[k] for s_ in stages), 1) for k in stages[0]}
+    desc = (f"{wl.name} G={G}, full workload, no extrapolation: all {wl.T * wl.k} pairs and all "
+            f"{wl.E} x {P} elements, {warmup} untimed + {iters} timed iterations ({n_tr}-iteration "
+            f"trace cycled, the GPU arm's t=0 synthetic grads); oracle/step.py OracleSim unchanged, the "
+            f"element range split over {C} worker processes pinned one per host core (each also runs "
+            f"the full a0/a2 dispatch and a1 plan); value = median wall time per iteration")
+    return {"ms": 1000.0 * statistics.median(walls), "per_iter_s": walls, "cores": C,
+            "stages_ms": st, "setup_s": round(setup_s, 1), "sample": desc}
+
+
+def oracle_leg_json(wl_name: str, G: int, warmup: int, iters: int, n_tr: int, workers: int | None) -> dict:
+    """The oracle leg in a child process (bench --oracle-leg): forking workers from a process
+    that holds a CUDA context is avoided."""
+    cmd = [sys.executable, os.path.abspath(__file__), "--oracle-leg", "--config", wl_name,
+           "--gpus", str(G), "--warmup", str(warmup), "--steps", str(iters), "--trace-iters", str(n_tr)]
+    if workers:
+        cmd += ["--oracle-workers", str(workers)]
+    env = dict(os.environ)
+    for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "LOCAL_WORLD_SIZE"):
+        env.pop(k, None)
+    r = subprocess.run(cmd, capture_output=True, text=True, env=env)
+    lines = [x for x in r.stdout.splitlines() if x.startswith("{")]
+    if r.returncode != 0 or not lines:
+        return {"error": (r.stderr or r.stdout)[-500:]}
+    return json.loads(lines[-1])
 
 
 def host_info() -> dict:
@@ -176,57 +268,29 @@ def host_info() -> dict:
                 break
     except OSError:
         pass
-    return {"cpu_model": model, "host_cores": os.cpu_count(), "pinned_cores": 1}
-
-
-def _run_oracle_sample(wl, G: int, iters: int, frac_den: int, seed_shift: int):
-    from oracle import dispatch as od
-    from oracle import plan as op
-    from oracle import step as ostep
-    from synth import configs, hashgen, traces
-    S = wl.S(G)
-    seed = configs.seed_for(wl.name) + seed_shift
-    idx = np.arange(0, wl.P, frac_den, dtype=np.int64)
-    sim = ostep.OracleSim(wl.E, G, S, wl.P, seed, idx=idx)
-    tr = traces.make_trace(wl, iters=iters)
-    per = []
-    for t, (ids, gates) in enumerate(tr):
-        ids_r, gates_r = traces.split_ranks(ids, G), traces.split_ranks(gates, G)
-        grads = {j: hashgen.grad_bits(seed, t, j, idx.astype(np.uint64)) for j in range(G * S)}
-        t0 = time.perf_counter()
-        disp = od.dispatch(ids_r, gates_r, sim.plan["first_slot"], wl.E)     # a0 + a2 (full)
-        op.plan(disp["C"], wl.E, G, S)                                     # a1 (full)
-        t1 = time.perf_counter()
-        sim.iterate(ids_r, gates_r, lambda j: grads[j])                    # a0..a5 (sampled elems)
-        t2 = time.perf_counter()
-        # sim.iterate repeats dispatch + plan on the full pair set: subtract that share
-        elementwise = max(0.0, (t2 - t1) - (t1 - t0))
-        per.append((t1 - t0) + elementwise * frac_den)
-    desc = (f"{wl.name} G={G}: full a0/a1/a2 on all {wl.T * wl.k} pairs; a3-a5 on every "
-            f"{frac_den}th element of all {wl.E} experts x {G * S} slots, extrapolated x{frac_den}")
-    return 1000.0 * statistics.median(per), desc, per
+    aff = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else None
+    return {"cpu_model": model, "host_cores": os.cpu_count(), "cores_available": aff}
 
 
 def reference_arm(args, wl):
     rank, world, _ = _env_rank()
     if rank != 0:
         return 0
-    import numpy as _np  # noqa: F401
     G = args.gpus
-    total = args.warmup + args.steps
     t0 = time.perf_counter()
-    ms, desc, per = run_oracle_sample(wl, G, total, frac_den=args.ref_frac)
-    timed = per[args.warmup:] if len(per) > args.warmup else per
-    val = 1000.0 * statistics.median(timed)
+    n_tr = min(args.warmup + args.steps, args.trace_iters)
+    r = run_oracle_full(wl, G, args.warmup, args.steps, n_tr, args.oracle_workers)
+    val = r["ms"]
     line = {
         "impl": "reference", "metric": METRIC, "value": round(val, 3), "unit": "ms/iter",
         "n_gpus": G, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(val, 3),
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "config": _config(wl, G),
-        "cpu_baseline": {"value": round(val, 3), "unit": "ms/iter", "cores": 1, "kind": "oracle",
-                         "sample": desc, "host": host_info()},
+        "cpu_baseline": {"value": round(val, 3), "unit": "ms/iter", "cores": r["cores"], "kind": "oracle",
+                         "sample": r["sample"], "stages_ms": r["stages_ms"], "host": host_info()},
         "e2e": {"value": round(val, 3), "unit": "ms/iter", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "timed_region_s": round(sum(r["per_iter_s"]), 1), "setup_s": r["setup_s"],
         "wall_s": round(time.perf_counter() - t0, 1),
     }
     print(json.dumps(line), flush=True)
@@ -377,6 +441,11 @@ def gpu_arm(args, wl):
     G = args.gpus
     if world != G:
         raise SystemExit(f"--gpus {G} but WORLD_SIZE={world}")
+    from synth import traces as _traces
+    n_tr = min(args.warmup + args.steps, args.trace_iters)
+    # input generation before any CUDA work (the pool forks); a local-rank share of the cores each
+    ncores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else 1
+    tr = _traces.make_trace(wl, iters=n_tr, workers=max(1, ncores // max(1, G)))
     torch.cuda.set_device(local)
     if G > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -400,8 +469,6 @@ def gpu_arm(args, wl):
                                  host_state=args.host_state, lazy_replicate=args.lazy)
     if G > 1:
         layer.connect()
-    n_tr = min(args.warmup + args.steps, args.trace_iters)
-    tr = traces.make_trace(wl, iters=n_tr)
     ids_d = [torch.from_numpy(traces.split_ranks(i, G)[rank].copy()).cuda() for i, _ in tr]
     gates_d = [torch.from_numpy(traces.split_ranks(g, G)[rank].copy()).cuda() for _, g in tr]
     api.synth_grads(layer.slot_g[0], seed, 0, rank * S, S, wl.P)
@@ -603,9 +670,12 @@ def gpu_arm(args, wl):
 
     cpu = None
     if rank == 0 and G == 1 and not args.no_cpu_baseline:
-        ms, desc, _ = run_oracle_sample(wl, G, args.cpu_iters, frac_den=args.cpu_frac)
-        cpu = {"value": round(ms, 1), "unit": "ms/iter", "cores": 1, "kind": "oracle", "sample": desc,
-               "host": host_info()}
+        r = oracle_leg_json(wl.name, G, 1, args.cpu_iters, n_tr, args.oracle_workers)
+        if "error" in r:
+            cpu = {"value": None, "unit": "ms/iter", "kind": "oracle", "error": r["error"]}
+        else:
+            cpu = {"value": round(r["ms"], 1), "unit": "ms/iter", "cores": r["cores"], "kind": "oracle",
+                   "sample": r["sample"], "stages_ms": r["stages_ms"], "host": host_info()}
 
     if rank == 0:
         line = {
@@ -649,7 +719,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="gpt-small")
+    ap.add_argument("--config", default="qwen3-fine",
+                    help="workload (synth/configs.py); the default is the largest single-GPU config")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--trace-iters", type=int, default=25)
     ap.add_argument("--e2e-steps", type=int, default=10)
@@ -667,9 +738,10 @@ def main():
     ap.add_argument("--host-state", action="store_true",
                     help="row f4: optimizer shards in pinned host memory (MOE_OPT_HOST_STATE)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-iters", type=int, default=3)
-    ap.add_argument("--cpu-frac", type=int, default=64)
-    ap.add_argument("--ref-frac", type=int, default=256)
+    ap.add_argument("--cpu-iters", type=int, default=3, help="timed oracle iterations of the cpu_baseline leg")
+    ap.add_argument("--oracle-workers", type=int, default=None,
+                    help="oracle worker processes (default: every available host core, <= 64)")
+    ap.add_argument("--oracle-leg", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--traffic", type=float, default=None,
                     help="dram bytes per k_update launch from an ncu --set full capture")
     args = ap.parse_args()
@@ -679,6 +751,10 @@ def main():
     args.lazy = args.dedup and args.lazy in ("auto", "on")
     from synth import configs
     wl = configs.CONFIGS[args.config]
+    if args.oracle_leg:   # child of the GPU arm's cpu_baseline (no CUDA in this process)
+        r = run_oracle_full(wl, args.gpus, args.warmup, args.steps, args.trace_iters, args.oracle_workers)
+        print(json.dumps(r), flush=True)
+        return 0
     if args.impl == "reference":
         return reference_arm(args, wl)
     return gpu_arm(args, wl)

@@ -230,10 +230,14 @@ int moe_ctx_get_timing_ex(moe_ctx *ctx, double *ms, int64_t *n);
 int moe_ctx_check(moe_ctx *ctx, void *stream);
 
 /* Blocks the calling host thread until the C_e of the most recent moe_dispatch have landed
- * in out->counts_host: the scan kernel's last block writes them to the pinned buffer and
- * releases a pinned host flag (system scope) that this call spins on -- BEFORE the scatter
- * kernel, so the host planner (step 6 may "execute earlier, even right after step 1",
- * PAPER.md:709 fn) overlaps the scatter.  MOE_OK if no dispatch was issued;
+ * in out->counts_host: a dispatch kernel writes them to the pinned buffer and releases a
+ * pinned host flag (system scope) that this call spins on -- the histogram kernel's last
+ * block when G == 1, the scan kernel's last block when G > 1 -- BEFORE the scatter kernel,
+ * so the host planner (step 6 may "execute earlier, even right after step 1", PAPER.md:709
+ * fn) overlaps the rest of the dispatch.  ONLY counts_host is guaranteed on return: every
+ * other output of the dispatch (counts_dev, slot_load, send_count, drops, the per-pair
+ * arrays) may still be in flight and needs ordinary stream ordering (work enqueued on the
+ * dispatch's stream, or an event on it).  MOE_OK if no dispatch was issued;
  * MOE_ERR_TIMEOUT after 30 s (e.g. a peer never arrived), MOE_ERR_CUDA on a sticky error. */
 int moe_ctx_wait_counts(moe_ctx *ctx);
 
@@ -275,7 +279,10 @@ typedef struct {
  * per-pair arrays may be NULL when T == 0), capacity < 0, a real-mode context not connected,
  * counts_host not pinned; MOE_ERR_SHAPE -- plan not a valid placement for the context.
  * Device-raised (reported by moe_ctx_check): MOE_ERR_DATA -- an id outside [0, E) or repeated
- * within a token (outputs undefined); MOE_ERR_TIMEOUT -- a peer's counts never arrived.    */
+ * within a token (outputs undefined); MOE_ERR_TIMEOUT -- a peer's counts never arrived: the
+ * scan and scatter kernels then write no outputs (the per-pair arrays keep stale contents,
+ * no memory outside them is touched), and every later dispatch does the same until
+ * moe_ctx_check has reported and cleared the error.                                      */
 int moe_dispatch(moe_ctx *ctx, const int32_t *topk_ids, const float *gates, int64_t T,
                  const moe_plan_t *plan, const moe_dispatch_out *out, void *stream);
 
@@ -309,8 +316,11 @@ int moe_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *plan_
  * One whole iteration, natively, in the paper's order (fig:design_diagram):
  *   moe_dispatch(plan_cur)                                   a0 + a2   (device, async)
  *   wait for C_t in out->counts_host (pinned; required)     (host spins on a pinned flag that
- *                                                             the scan kernel releases; the
- *                                                             scatter kernel keeps running)
+ *                                                             the histogram (G == 1) or scan
+ *                                                             (G > 1) kernel releases; the
+ *                                                             rest of the dispatch keeps
+ *                                                             running -- only counts_host is
+ *                                                             complete at that point)
  *   moe_plan_ex(C_t, policy) -> *plan_next                   a1        (host C++; "may execute
  *                                                             earlier, even right after
  *                                                             step 1", PAPER.md:709 fn)

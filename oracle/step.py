@@ -19,6 +19,8 @@ configs are checked on sampled elements.
 """
 from __future__ import annotations
 
+import time
+
 import numpy as np
 
 from . import adam as _adam
@@ -83,25 +85,42 @@ class OracleSim:
         self.plan = _plan.plan(np.ones(E, dtype=np.int64), E, G, S, policy)
         self.w_slot = place(self.master, self.plan["slot_expert"])
         self.step = 1
+        # wall seconds per stage of the last iterate() (bench.py's cpu_baseline breakdown;
+        # instrumentation only, no effect on any value)
+        self.stage_s: dict = {}
 
     def iterate(self, ids_per_rank, gates_per_rank, grad_of_slot) -> dict:
         """grad_of_slot(j) -> uint16 bf16 bits of global slot j's grad over ``idx``."""
         E, G, S = self.E, self.G, self.S
         plan_t = self.plan
+        clk = [time.perf_counter()]
         disp = _dispatch.dispatch(ids_per_rank, gates_per_rank, plan_t["first_slot"], E,
                                   self.capacity)                                            # a0, a2
+        clk.append(time.perf_counter())
         if self.step % self.replan_interval == 0:
             plan_next = _plan.plan(disp["C"], E, G, S, self.policy)                        # a1
         else:  # interval policy (reading B3): keep the placement until the next re-plan
             plan_next = plan_t
+        clk.append(time.perf_counter())
         sc = _adam.scalars(self.hyper, self.step)
+        t_red = t_adam = 0.0
         for e in range(E):
+            t0 = time.perf_counter()
             g = reduce_expert(grad_of_slot, plan_t["first_slot"], e, S,
                               self.scale_mode, self.scale)                                  # a3
+            t1 = time.perf_counter()
             self.master[e], self.m[e], self.v[e] = _adam.adam_update(
                 self.master[e], self.m[e], self.v[e], g, sc)                                # a4
+            t_red += t1 - t0
+            t_adam += time.perf_counter() - t1
+        clk.append(time.perf_counter())
         self.w_slot = place(self.master, plan_next["slot_expert"])                          # a5
+        clk.append(time.perf_counter())
         self._check(disp, plan_next, ids_per_rank)
+        clk.append(time.perf_counter())
+        self.stage_s = {"a0_a2_dispatch": clk[1] - clk[0], "a1_plan": clk[2] - clk[1],
+                        "a3_reduce": t_red, "a4_adam": t_adam, "a5_place": clk[4] - clk[3],
+                        "invariant_checks": clk[5] - clk[4]}
         self.plan = plan_next
         self.step += 1
         return {"dispatch": disp, "plan_next": plan_next, "plan_cur": plan_t}

@@ -47,53 +47,79 @@ struct HistArgs {
 };
 
 __global__ void __launch_bounds__(kThreads) k_hist(const __grid_constant__ HistArgs a) {
-  __shared__ int32_t hist[MOE_MAX_E];
+  constexpr int kWarps = kThreads / 32;
+  __shared__ int32_t whist[kWarps][MOE_MAX_E];  // per-warp histograms (no cross-warp conflicts)
   __shared__ int is_last;
-  const int v = blockIdx.x / a.nb;   // local rank
-  const int b = blockIdx.x % a.nb;   // tile
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int v = blockIdx.y;   // local rank
+  const int b = blockIdx.x;   // tile
+  const int tid = threadIdx.x, warp = tid >> 5;
   const int32_t *ids = a.ids + (int64_t)v * a.npairs;
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // let k_scan get scheduled
-  for (int e = tid; e < a.E; e += kThreads) hist[e] = 0;
+  for (int i = tid; i < kWarps * MOE_MAX_E; i += kThreads) (&whist[0][0])[i] = 0;
   __syncthreads();
 
   const int64_t t0 = (int64_t)b * a.tile;
-#pragma unroll 4
-  for (int i = 0; i < a.tile / kThreads; ++i) {
-    const int64_t p = t0 + i * kThreads + tid;
-    const bool in = p < a.npairs;
-    int e = in ? __ldg(ids + p) : -1;
-    bool valid = in && (unsigned)e < (unsigned)a.E;
-    if (in && !valid) atomicOr(a.err, kErrData);
-    // the k experts of a token must be distinct.  k | 32: a token's pairs are k aligned lanes
-    // of this warp (tiles and rounds start at multiples of 32), so the expert-match mask
-    // below answers it; otherwise re-read the token's earlier ids.
-    if (valid && a.k > 1 && (32 % a.k) != 0) {
-      const int j = (int)(p % a.k);
-      for (int jj = 0; jj < j; ++jj)
-        if (__ldg(ids + (p - j + jj)) == e) atomicOr(a.err, kErrData);
+  const int n = (int)min((int64_t)a.tile, a.npairs - t0);
+  const int32_t *tp = ids + t0;
+  int32_t *wh = whist[warp];
+  bool bad = false;
+  // Histogram: 4 consecutive ids per thread per step (one 16-byte load when aligned).
+  const bool vec = (((uintptr_t)tp) & 15) == 0;
+  for (int i = tid * 4; i < n; i += kThreads * 4) {
+    int e4[4];
+    if (vec && i + 4 <= n) {
+      const int4 x = __ldg(reinterpret_cast<const int4 *>(tp + i));
+      e4[0] = x.x; e4[1] = x.y; e4[2] = x.z; e4[3] = x.w;
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) e4[u] = i + u < n ? __ldg(tp + i + u) : 0;
     }
-    const unsigned act = __ballot_sync(0xffffffffu, valid);
-    if (valid) {
-      const unsigned peers = __match_any_sync(act, e);
-      if (a.k > 1 && (32 % a.k) == 0) {
-        const unsigned tok = (a.k == 32 ? 0xffffffffu : ((1u << a.k) - 1u)) << (lane / a.k * a.k);
-        if (__popc(peers & tok) > 1) atomicOr(a.err, kErrData);
-      }
-      if (lane == __ffs(peers) - 1) atomicAdd(&hist[e], __popc(peers));
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (i + u >= n) break;
+      if ((unsigned)e4[u] < (unsigned)a.E) atomicAdd(&wh[e4[u]], 1);
+      else bad = true;
     }
   }
+  // The k experts of a token must be distinct: every token whose first pair lies in this tile
+  // is checked pairwise (its ids were just read: L1 hits).
+  if (a.k > 1) {
+    const int64_t tok0 = (t0 + a.k - 1) / a.k, tok1 = (t0 + n + a.k - 1) / a.k;
+    for (int64_t t = tok0 + tid; t < tok1; t += kThreads) {
+      const int32_t *q = ids + t * a.k;
+      if (a.k <= 8) {  // registers, unrolled; absent positions get distinct negative sentinels
+        int32_t x[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = j < a.k ? __ldg(q + j) : -1 - j;
+#pragma unroll
+        for (int j = 1; j < 8; ++j)
+#pragma unroll
+          for (int jj = 0; jj < j; ++jj) bad |= x[j] == x[jj];
+      } else {
+        for (int j = 1; j < a.k; ++j) {
+          const int32_t y = __ldg(q + j);
+          for (int jj = 0; jj < j; ++jj) bad |= y == __ldg(q + jj);
+        }
+      }
+    }
+  }
+  if (bad) atomicOr(a.err, kErrData);
   __syncthreads();
 
   int32_t *blk = a.blk + (int64_t)v * a.E * a.nb_max;
   for (int e = tid; e < a.E; e += kThreads) {
-    const int32_t h = hist[e];
+    int32_t h = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) h += whist[w][e];
     blk[(int64_t)e * a.nb_max + b] = h;
     if (h) atomicAdd(a.cnt_local + v * a.E + e, h);
   }
-  __threadfence();
+  // ticket: bar.sync orders the block's writes before thread 0's (cumulative) fence
   __syncthreads();
-  if (tid == 0) is_last = (atomicAdd(a.done + v, 1u) == (unsigned)(a.nb - 1));
+  if (tid == 0) {
+    __threadfence();
+    is_last = (atomicAdd(a.done + v, 1u) == (unsigned)(a.nb - 1));
+  }
   __syncthreads();
   if (!is_last) return;
 
@@ -114,9 +140,9 @@ __global__ void __launch_bounds__(kThreads) k_hist(const __grid_constant__ HistA
   const bool host = a.G == 1 && a.counts_host != nullptr;  // C_e = this rank's counts
   if (host)
     for (int e = tid; e < a.E; e += kThreads) a.counts_host[e] = a.dst[0]->xcnt[a.parity][grank][e];
-  if (flags || host) __threadfence_system();
   __syncthreads();
   if (tid == 0) {
+    if (flags || host) __threadfence_system();
     a.done[v] = 0;
     if (flags)
       for (int h = 0; h < a.G; ++h) st_release_sys(&a.dst[h]->disp_flag[grank], a.epoch);
@@ -191,7 +217,10 @@ __global__ void __launch_bounds__(kThreads) k_scan(const __grid_constant__ ScanA
         if (!wait_flag(&a.sync->disp_flag[h], a.epoch, a.err)) ok = 0;
   }
   __syncthreads();
-  if (!ok) return;
+  // A peer's counts never arrived (timeout bit raised): compute nothing -- k_scatter sees the
+  // bit and writes nothing either -- but still take (and reset) the block ticket below, so the
+  // next dispatch finds the counter at zero.  The context stays poisoned until moe_ctx_check.
+  if (ok) {
   if (warp == 0) {  // warp-parallel: C_e and this rank's base over GPUs
     const int32_t(*x)[MOE_MAX_E] = a.sync->xcnt[a.parity];
     const int32_t c = lane < a.G ? ld_cg(&x[lane][e]) : 0;
@@ -267,6 +296,7 @@ __global__ void __launch_bounds__(kThreads) k_scan(const __grid_constant__ ScanA
     row[i] = run;
     run += c;
   }
+  }  // ok
 
   // The last block publishes C_t to the host (threadfence-reduction pattern): every block
   // orders its counts_dev write before its ticket (GPU scope); the last one copies the E
@@ -281,7 +311,8 @@ __global__ void __launch_bounds__(kThreads) k_scan(const __grid_constant__ ScanA
   __syncthreads();
   if (s_last) {
     __threadfence();
-    const bool publish = a.G > 1 || !a.counts_host;  // on one GPU k_hist already did
+    const bool publish = (a.G > 1 || !a.counts_host) &&   // on one GPU k_hist already did
+                         !(__ldcg(a.err) & kErrTimeout);   // never release incomplete counts
     if (publish && a.counts_host)
       for (int x = tid; x < a.E; x += kThreads) a.counts_host[x] = __ldcg(a.counts_dev + x);
     __syncthreads();
@@ -296,6 +327,7 @@ __global__ void __launch_bounds__(kThreads) k_scan(const __grid_constant__ ScanA
 }
 
 struct ScatterArgs {
+  int32_t *err;
   const int32_t *ids;
   const float *gates;
   int64_t npairs;
@@ -308,27 +340,54 @@ struct ScatterArgs {
   int32_t fs[MOE_MAX_E + 1];
 };
 
+// Dynamic shared memory of k_scatter for a tile of `tile` pairs and G*S slots.
+__host__ __device__ constexpr size_t scatter_smem(int tile, int GS) {
+  return (size_t)tile * (4 + 4 + 4 + 2) + (size_t)GS * 4 + 16;
+}
+
 __global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ ScatterArgs a) {
   constexpr int kWarps = kThreads / 32;
-  __shared__ int32_t wcnt[kWarps][MOE_MAX_E];
+  __shared__ int16_t wcnt[kWarps][MOE_MAX_E];  // per-warp running counts (< tile <= 4096)
   __shared__ ExpertInfo s_info[MOE_MAX_E];
   __shared__ int32_t s_blk[MOE_MAX_E];
-  __shared__ int32_t s_loc[MOE_MAX_E];  // where expert e's kept pairs start in this rank's send order
+  __shared__ int32_t s_loc[MOE_MAX_E];   // where expert e's kept pairs start in this rank's send order
+  __shared__ int32_t s_toff[MOE_MAX_E];  // where expert e's pairs start in this tile's expert-sorted order
   __shared__ int32_t s_fs[MOE_MAX_E + 1];  // plan_t (lane-divergent reads: not from the param bank)
-  extern __shared__ int32_t s_tile[];  // [tile] ids, then [tile] gates (bit patterns)
-  const int v = blockIdx.x / a.nb;
-  const int b = blockIdx.x % a.nb;
+  __shared__ int s_poisoned;
+  extern __shared__ __align__(16) int32_t s_dyn[];
+  int32_t *s_tile = s_dyn;                     // [tile] ids, then (rank << 8 | e) after pass 1
+  int32_t *s_gate = s_dyn + a.tile;            // [tile] gate bit patterns
+  int32_t *st_pos = s_dyn + 2 * a.tile;        // [tile] send position (or -1), expert-sorted order
+  int32_t *s_kp = s_dyn + 3 * a.tile;          // [GS] kept_pre of this rank
+  uint16_t *st_pair = reinterpret_cast<uint16_t *>(s_dyn + 3 * a.tile + a.GS);  // [tile] pair in tile
+  const int v = blockIdx.y;
+  const int b = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t off_v = (int64_t)v * a.npairs;
+  const int64_t tbase = (int64_t)b * a.tile;
+  const int n = (int)min((int64_t)a.tile, a.npairs - tbase);
   {  // stage the tile's ids and gates (inputs, not produced by k_scan): independent, coalesced
-    const int64_t t0 = (int64_t)b * a.tile;
-    const int n = (int)(a.npairs - t0 < a.tile ? a.npairs - t0 : a.tile);
-    for (int i = tid; i < n; i += kThreads) {
-      s_tile[i] = __ldg(a.ids + off_v + t0 + i);
-      s_tile[a.tile + i] = __float_as_int(__ldg(a.gates + off_v + t0 + i));
+    const int32_t *ip = a.ids + off_v + tbase;
+    const int32_t *gp = reinterpret_cast<const int32_t *>(a.gates) + off_v + tbase;
+    if ((((uintptr_t)ip | (uintptr_t)gp) & 15) == 0) {
+      const int n4 = n >> 2;
+      for (int i = tid; i < n4; i += kThreads) {
+        reinterpret_cast<int4 *>(s_tile)[i] = __ldg(reinterpret_cast<const int4 *>(ip) + i);
+        reinterpret_cast<int4 *>(s_gate)[i] = __ldg(reinterpret_cast<const int4 *>(gp) + i);
+      }
+      for (int i = 4 * n4 + tid; i < n; i += kThreads) {
+        s_tile[i] = __ldg(ip + i);
+        s_gate[i] = __ldg(gp + i);
+      }
+    } else {
+      for (int i = tid; i < n; i += kThreads) {
+        s_tile[i] = __ldg(ip + i);
+        s_gate[i] = __ldg(gp + i);
+      }
     }
   }
-  pdl_wait();  // k_scan's outputs (einfo, scanned tile counts)
+  pdl_wait();  // k_scan's outputs (einfo, scanned tile counts, kept_pre)
+  if (tid == 0) s_poisoned = (__ldcg(a.err) & kErrTimeout) != 0;  // k_scan timed out: no outputs
   for (int e = tid; e < a.E; e += kThreads) {
     s_info[e] = a.einfo[v * a.E + e];
     s_blk[e] = a.blk[((int64_t)v * a.E + e) * a.nb_max + b];
@@ -336,7 +395,9 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ Sc
     for (int w = 0; w < kWarps; ++w) wcnt[w][e] = 0;
   }
   for (int e = tid; e <= a.E; e += kThreads) s_fs[e] = a.fs[e];
+  for (int j = tid; j < a.GS; j += kThreads) s_kp[j] = a.kept_pre[(int64_t)v * a.GS + j];
   __syncthreads();
+  if (s_poisoned) return;
   if (warp == 0) {  // s_loc = exclusive prefix over experts of this rank's kept counts
     constexpr int kPer = MOE_MAX_E / 32;
     int32_t c[kPer], s = 0;
@@ -360,9 +421,7 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ Sc
       run += c[i];
     }
   }
-  __syncthreads();
   const int32_t capv = a.cap > 0 ? a.cap : 0x7fffffff;
-  const int32_t *kept_pre = a.kept_pre + (int64_t)v * a.GS;
 
   // Warp w owns the consecutive pairs [w*R*32, (w+1)*R*32) of the tile (R = tile/256 rounds of
   // 32): pair order == (warp, round, lane) order, so the ranks below are stable.
@@ -371,13 +430,12 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ Sc
   // and packs (rank << 8 | e) into the staged id; an exclusive prefix over warps then turns
   // the per-warp totals into starting ranks, and pass 2 needs no further matching.
   const int rounds = a.tile / kThreads;
-  const int64_t seg = (int64_t)b * a.tile + (int64_t)warp * rounds * 32;
+  const int seg = warp * rounds * 32;
   const unsigned lt = (1u << lane) - 1u;
-  const int64_t tbase = (int64_t)b * a.tile;
   for (int r = 0; r < rounds; ++r) {  // pass 1
-    const int64_t p = seg + r * 32 + lane;
-    const bool in = p < a.npairs;
-    const int e = in ? s_tile[p - tbase] : -1;
+    const int p = seg + r * 32 + lane;
+    const bool in = p < n;
+    const int e = in ? s_tile[p] : -1;
     const bool valid = in && (unsigned)e < (unsigned)a.E;
     const unsigned act = __ballot_sync(0xffffffffu, valid);
     unsigned peers = 0;
@@ -387,34 +445,65 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ Sc
       wr = wcnt[warp][e] + __popc(peers & lt);
     }
     __syncwarp();
-    if (valid && lane == __ffs(peers) - 1) wcnt[warp][e] += __popc(peers);
-    if (in) s_tile[p - tbase] = valid ? (wr << 8) | e : -1;  // E <= 256, wr < tile
+    if (valid && lane == __ffs(peers) - 1) wcnt[warp][e] = (int16_t)(wcnt[warp][e] + __popc(peers));
+    if (in) s_tile[p] = valid ? (wr << 8) | e : -1;  // E <= 256, wr < tile
     __syncwarp();
   }
   __syncthreads();
-  for (int e = tid; e < a.E; e += kThreads) {  // exclusive prefix over warps, per expert
+  // exclusive prefix over warps, per expert (-> starting rank of each warp's pairs of e inside
+  // the tile), and the tile's count of e
+  __shared__ int32_t s_tcnt[MOE_MAX_E];
+  for (int e = tid; e < a.E; e += kThreads) {
     int32_t run = 0;
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) {
       const int32_t c = wcnt[w][e];
-      wcnt[w][e] = run;
+      wcnt[w][e] = (int16_t)run;
       run += c;
+    }
+    s_tcnt[e] = run;
+  }
+  __syncthreads();
+  if (warp == 0) {  // s_toff = exclusive prefix over experts of the tile counts
+    constexpr int kPer = MOE_MAX_E / 32;
+    int32_t c[kPer], s = 0;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const int e = lane * kPer + i;
+      c[i] = e < a.E ? s_tcnt[e] : 0;
+      s += c[i];
+    }
+    int32_t incl = s;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += y;
+    }
+    int32_t run = incl - s;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const int e = lane * kPer + i;
+      if (e < a.E) s_toff[e] = run;
+      run += c[i];
     }
   }
   __syncthreads();
-  for (int r = 0; r < rounds; ++r) {  // pass 2
-    const int64_t p = seg + r * 32 + lane;
-    if (p >= a.npairs) break;
-    const int32_t x = s_tile[p - tbase];
+  // Pass 2: per pair (slot, offset) -- written in pair order (coalesced) -- and its send
+  // position, staged in the tile's expert-sorted order (stable: rank order within e).
+  int32_t *dslot = a.dest_slot + off_v + tbase, *doff = a.dest_off + off_v + tbase;
+  for (int r = 0; r < rounds; ++r) {
+    const int p = seg + r * 32 + lane;
+    if (p >= n) break;
+    const int32_t x = s_tile[p];
     if (x < 0) {  // invalid id: flagged by k_hist; keep memory safe
-      a.dest_slot[off_v + p] = -1;
-      a.dest_off[off_v + p] = -1;
+      dslot[p] = -1;
+      doff[p] = -1;
       continue;
     }
     const int e = x & 0xff;
-    const int32_t wr = wcnt[warp][e] + (x >> 8);
+    const int32_t tr = wcnt[warp][e] + (x >> 8);  // rank of the pair among the tile's pairs of e
     const ExpertInfo info = s_info[e];
-    const int32_t lr = s_blk[e] + wr;  // rank within this rank's pairs of e
+    const int32_t lr = s_blk[e] + tr;  // rank within this rank's pairs of e
     const int32_t R = info.base + lr;  // global rank within expert e
     const int32_t q = info.q, m = info.m;
     const int32_t big = m * (q + 1);
@@ -422,20 +511,32 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ Sc
                                 : m + (int32_t)udiv_fast((uint32_t)(R - big), (uint32_t)q, info.rq);
     const int32_t start = rho * q + min(rho, m);
     const int32_t off = R - start;
+    const int32_t si = s_toff[e] + tr;
+    st_pair[si] = (uint16_t)p;
     if (off >= capv) {  // row f2: beyond the replica's capacity -> dropped, not sent
-      a.dest_slot[off_v + p] = -1;
-      a.dest_off[off_v + p] = -1;
+      dslot[p] = -1;
+      doff[p] = -1;
+      st_pos[si] = -1;
       continue;
     }
     const int32_t slot = s_fs[e] + rho;
-    a.dest_slot[off_v + p] = slot;
-    a.dest_off[off_v + p] = off;
+    dslot[p] = slot;
+    doff[p] = off;
     // slot-major position among this rank's kept pairs: experts before e, kept pairs of this
     // rank in e's earlier replicas, then this rank's pairs in replica rho before this one
     // (all kept: a replica keeps a prefix of its offsets)
-    const int64_t pos = off_v + s_loc[e] + __ldg(kept_pre + slot) + (R - max(info.base, start));
-    a.send_pair[pos] = (int32_t)p;
-    a.send_gate[pos] = __int_as_float(s_tile[a.tile + (p - tbase)]);
+    st_pos[si] = s_loc[e] + s_kp[slot] + (R - max(info.base, start));
+  }
+  __syncthreads();
+  // Pass 3: send_pair / send_gate in the expert-sorted order.  Consecutive sorted entries of one
+  // expert go to consecutive send positions, so the stores form contiguous runs.
+  const int nsorted = s_toff[a.E - 1] + s_tcnt[a.E - 1];  // valid pairs of the tile
+  for (int i = tid; i < nsorted; i += kThreads) {
+    const int32_t pos = st_pos[i];
+    if (pos < 0) continue;
+    const int p = st_pair[i];
+    a.send_pair[off_v + pos] = (int32_t)(tbase + p);
+    a.send_gate[off_v + pos] = __int_as_float(s_gate[p]);
   }
 }
 
@@ -447,10 +548,10 @@ using namespace moe;
 int moe_validate_plan(const moe_ctx *ctx, const moe_plan_t *p, const char *what);  // ctx.cu
 
 // Per-device kernel attributes of the dispatch (called by moe_ctx_create on ctx->device):
-// k_scatter's static smem (~17 KB) + 2 x tile ints of staged ids/gates can exceed 48 KB.
+// k_scatter's static smem (~20 KB) + its staged tile (14 B/pair) + kept_pre can exceed 48 KB.
 int moe_dispatch_init() {
   MOE_CUDA_TRY(cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)(2 * kMaxTilePairs * sizeof(int32_t))));
+                                    (int)scatter_smem(kMaxTilePairs, MOE_MAX_SLOTS)));
   return MOE_OK;
 }
 
@@ -500,9 +601,20 @@ extern "C" int moe_dispatch(moe_ctx *ctx, const int32_t *topk_ids, const float *
   tile = std::max<int64_t>(kTilePairs, (tile + kThreads - 1) / kThreads * kThreads);
   tile = std::min<int64_t>(tile, kMaxTilePairs);  // k_scatter stages ids + gates in smem
   const int nb = (int)std::max<int64_t>(1, (npairs + tile - 1) / tile);
+  const int real = ctx->rank >= 0 ? 1 : 0;
+  int64_t *counts_host_dev = nullptr;
+  if (out->counts_host) {  // C_t goes straight to pinned host memory (PAPER.md:709 fn: plan early)
+    void *dptr = nullptr;
+    if (cudaHostGetDevicePointer(&dptr, out->counts_host, 0) != cudaSuccess || !dptr) {
+      cudaGetLastError();
+      return fail(MOE_ERR_INVALID, "moe_dispatch: counts_host must be pinned (page-locked) host memory");
+    }
+    counts_host_dev = (int64_t *)dptr;
+  }
+  // the exchange epoch advances only after every check that can reject the call: a rank that
+  // returned early must not run ahead (its flag at e+1 would satisfy a peer waiting for e)
   const uint32_t epoch = ++ctx->disp_epoch;
   const int parity = (int)(epoch & 1u);
-  const int real = ctx->rank >= 0 ? 1 : 0;
 
   HistArgs ha{};
   ha.ids = topk_ids;
@@ -522,19 +634,10 @@ extern "C" int moe_dispatch(moe_ctx *ctx, const int32_t *topk_ids, const float *
   ha.done = ctx->done;
   ha.err = ctx->err;
   for (int h = 0; h < MOE_MAX_G; ++h) ha.dst[h] = real ? ctx->peer_sync[h] : ctx->sync;
-  int64_t *counts_host_dev = nullptr;
-  if (out->counts_host) {  // C_t goes straight to pinned host memory (PAPER.md:709 fn: plan early)
-    void *dptr = nullptr;
-    if (cudaHostGetDevicePointer(&dptr, out->counts_host, 0) != cudaSuccess || !dptr) {
-      cudaGetLastError();
-      return fail(MOE_ERR_INVALID, "moe_dispatch: counts_host must be pinned (page-locked) host memory");
-    }
-    counts_host_dev = (int64_t *)dptr;
-  }
   ha.counts_host = counts_host_dev;
   ha.host_flag = ctx->host_flag_dev;
   const auto tev = timing_begin(ctx, s);
-  k_hist<<<nb * ctx->n_local, kThreads, 0, s>>>(ha);
+  k_hist<<<dim3(nb, ctx->n_local), kThreads, 0, s>>>(ha);
   MOE_CUDA_TRY(cudaGetLastError());
 
   ScanArgs sa{};
@@ -565,6 +668,7 @@ extern "C" int moe_dispatch(moe_ctx *ctx, const int32_t *topk_ids, const float *
   ctx->counts_pending = true;
 
   ScatterArgs ca{};
+  ca.err = ctx->err;
   ca.ids = topk_ids;
   ca.gates = gates;
   ca.npairs = npairs;
@@ -583,7 +687,7 @@ extern "C" int moe_dispatch(moe_ctx *ctx, const int32_t *topk_ids, const float *
   ca.kept_pre = ctx->kept_pre;
   for (int e = 0; e <= ctx->E; ++e) ca.fs[e] = plan->first_slot[e];
   if (npairs > 0)
-    MOE_CUDA_TRY(launch_pdl(k_scatter, dim3(nb * ctx->n_local), s, ca, (size_t)2 * tile * sizeof(int32_t)));
+    MOE_CUDA_TRY(launch_pdl(k_scatter, dim3(nb, ctx->n_local), s, ca, scatter_smem((int)tile, ctx->G * ctx->S)));
   timing_end(ctx->ev_disp, tev, s);
   return MOE_OK;
 }

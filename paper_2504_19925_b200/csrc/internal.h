@@ -16,7 +16,7 @@ namespace moe {
 
 constexpr int kThreads = 256;          // block size of every hot kernel
 constexpr int kTilePairs = 512;        // minimum dispatch tile: 8 warps x 2 rounds x 32 lanes
-constexpr int kMaxTilePairs = 4096;    // maximum (k_scatter stages 8 B/pair in shared memory)
+constexpr int kMaxTilePairs = 4096;    // maximum (k_scatter stages 14 B/pair in shared memory)
 constexpr int kVec = 8;                // elements per thread in the update (16 B of bf16)
 constexpr int kChunk = kThreads * kVec;  // update chunk: 2048 elements of one expert
 constexpr uint64_t kSpinTimeoutNs = 20ull * 1000 * 1000 * 1000;  // 20 s

@@ -118,6 +118,29 @@ __device__ __forceinline__ void place_to(const UpdArgs &a, int e, int owner, int
   }
 }
 
+__device__ __forceinline__ void st_stream8(uint16_t *p, const uint2 &v) {
+  asm volatile("st.global.cs.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(v.x), "r"(v.y) : "memory");
+}
+
+// a5 for k_update_tma's split mapping: 4 bf16 at element gi and (if has_b) 4 at gi + kChunk/2,
+// into the same slots as place_to.
+__device__ __forceinline__ void place_split(const UpdArgs &a, int e, int owner, int64_t gi,
+                                            const uint2 &wa, const uint2 &wbv, bool has_b) {
+  const int n0 = a.fs_next[e], n1 = a.fs_next[e + 1];
+  int h = a.h_first_next[e], l = n0 - h * a.S;
+  for (int j = n0; j < n1; ++j) {
+    if (!a.dedup || h == owner || j == n0 || l == 0) {
+      uint16_t *dst = a.wbase[h] + (int64_t)l * a.P + gi;
+      st_stream8(dst, wa);
+      if (has_b) st_stream8(dst + kChunk / 2, wbv);
+    }
+    if (++l == a.S) {
+      l = 0;
+      ++h;
+    }
+  }
+}
+
 // a4: Adam on 8 elements, reading A15 op order, IEEE fp32 RN per op, bf16 RNE out.
 __device__ __forceinline__ void adam8(const UpdArgs &a, const float (&tot)[8], float sc, float (&w)[8],
                                       float (&m)[8], float (&v)[8], uint4 &wb) {
@@ -426,6 +449,12 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_update_tma(const __grid_cons
   }
 
   // ---------------- consumers ----------------
+  // Element mapping: thread t owns the two 4-element groups [4t, 4t+4) and [H + 4t, H + 4t + 4)
+  // of the chunk (H = kChunk / 2), so every warp-wide access -- state float4 loads from the
+  // ring, state float4 stores, 8-byte bf16 weight stores -- covers one contiguous, fully
+  // written run of 512 or 256 bytes (the earlier 8-contiguous-elements mapping issued half-
+  // sector stores: 1.7x the store sectors the data needs).  Results do not depend on it.
+  constexpr int H = kChunk / 2;
   const int tid = threadIdx.x;
   uint32_t si = 0, gi_ = 0;
   for (;;) {
@@ -437,48 +466,42 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_update_tma(const __grid_cons
     const int64_t rem = it - (int64_t)(o - a.o_begin) * per_owner;
     const int e = (int)(rem % a.E);
     const int64_t c = a.c_lo + rem / a.E;
-    const int64_t loc = c * kChunk + (int64_t)tid * kVec;
-    const bool act = loc < a.Pg;
+    const int64_t loc = c * kChunk + (int64_t)tid * 4;  // group A; group B at loc + H
+    const bool act_a = loc < a.Pg, act_b = loc + H < a.Pg;  // (P/G) % 8 == 0: groups are whole
     float w[8], m[8], v[8];
     {
-      if (act) {
-        const float *src = state + (size_t)s * 3 * kChunk + tid * kVec;
-        const float4 w0 = *reinterpret_cast<const float4 *>(src);
-        const float4 w1 = *reinterpret_cast<const float4 *>(src + 4);
-        const float4 m0 = *reinterpret_cast<const float4 *>(src + kChunk);
-        const float4 m1 = *reinterpret_cast<const float4 *>(src + kChunk + 4);
-        const float4 v0 = *reinterpret_cast<const float4 *>(src + 2 * kChunk);
-        const float4 v1 = *reinterpret_cast<const float4 *>(src + 2 * kChunk + 4);
-        w[0] = w0.x; w[1] = w0.y; w[2] = w0.z; w[3] = w0.w; w[4] = w1.x; w[5] = w1.y; w[6] = w1.z; w[7] = w1.w;
-        m[0] = m0.x; m[1] = m0.y; m[2] = m0.z; m[3] = m0.w; m[4] = m1.x; m[5] = m1.y; m[6] = m1.z; m[7] = m1.w;
-        v[0] = v0.x; v[1] = v0.y; v[2] = v0.z; v[3] = v0.w; v[4] = v1.x; v[5] = v1.y; v[6] = v1.z; v[7] = v1.w;
-      }
+      const float *src = state + (size_t)s * 3 * kChunk + tid * 4;
+      const float4 w0 = *reinterpret_cast<const float4 *>(src);
+      const float4 w1 = *reinterpret_cast<const float4 *>(src + H);
+      const float4 m0 = *reinterpret_cast<const float4 *>(src + kChunk);
+      const float4 m1 = *reinterpret_cast<const float4 *>(src + kChunk + H);
+      const float4 v0 = *reinterpret_cast<const float4 *>(src + 2 * kChunk);
+      const float4 v1 = *reinterpret_cast<const float4 *>(src + 2 * kChunk + H);
+      w[0] = w0.x; w[1] = w0.y; w[2] = w0.z; w[3] = w0.w; w[4] = w1.x; w[5] = w1.y; w[6] = w1.z; w[7] = w1.w;
+      m[0] = m0.x; m[1] = m0.y; m[2] = m0.z; m[3] = m0.w; m[4] = m1.x; m[5] = m1.y; m[6] = m1.z; m[7] = m1.w;
+      v[0] = v0.x; v[1] = v0.y; v[2] = v0.z; v[3] = v0.w; v[4] = v1.x; v[5] = v1.y; v[6] = v1.z; v[7] = v1.w;
       release_slot(st_empty + s, lane);
       ++si;
     }
     // a3: two-level fp32 sum, replica slices in ascending slot order (reading A11)
     // For each GPU h hosting e (ascending): part = fp32 sum of its replica slices in ascending
     // slot order (or, de-duplicated, GPU h's precomputed fp32 partial -- the same value);
-    // tot = part_{h0} + part_{h1} + ... in ascending h.
+    // tot = part_{h0} + part_{h1} + ... in ascending h.  (Lanes of a ragged chunk's missing
+    // groups compute on stale ring bytes and store nothing.)
     const int j0 = a.fs_cur[e], j1 = a.fs_cur[e + 1];
     float part[8], tot[8];
     bool have_tot = false;
     for (int h = a.h_first_cur[e], ja = j0; ja < j1; ++h) {
       const int jb = min(j1, (h + 1) * a.S);
       const int q = (a.dedup && h != o) ? a.pq[e][h] : -1;
-      if (q >= 0) {
+      if (q >= 0) {  // fp32 partial: elements [0, H) in ring slot gA, [H, kChunk) in gB
         const int gA = gi_ % kGradSlots, gB = (gi_ + 1) % kGradSlots;
         mbar_wait(gr_full + gA, (gi_ / kGradSlots) & 1);
         mbar_wait(gr_full + gB, ((gi_ + 1) / kGradSlots) & 1);
-        if (act) {
-          const int half = tid >= kThreads / 2;
-          const float *src = reinterpret_cast<const float *>(grad + (size_t)(half ? gB : gA) * kChunk) +
-                             (tid - half * (kThreads / 2)) * kVec;
-          const float4 x0 = *reinterpret_cast<const float4 *>(src);
-          const float4 x1 = *reinterpret_cast<const float4 *>(src + 4);
-          part[0] = x0.x; part[1] = x0.y; part[2] = x0.z; part[3] = x0.w;
-          part[4] = x1.x; part[5] = x1.y; part[6] = x1.z; part[7] = x1.w;
-        }
+        const float4 x0 = *reinterpret_cast<const float4 *>(reinterpret_cast<const float *>(grad + (size_t)gA * kChunk) + tid * 4);
+        const float4 x1 = *reinterpret_cast<const float4 *>(reinterpret_cast<const float *>(grad + (size_t)gB * kChunk) + tid * 4);
+        part[0] = x0.x; part[1] = x0.y; part[2] = x0.z; part[3] = x0.w;
+        part[4] = x1.x; part[5] = x1.y; part[6] = x1.z; part[7] = x1.w;
         release_slot(gr_empty + gA, lane);
         release_slot(gr_empty + gB, lane);
         gi_ += 2;
@@ -486,35 +509,33 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_update_tma(const __grid_cons
         for (int j = ja; j < jb; ++j) {
           const int g = gi_ % kGradSlots;
           mbar_wait(gr_full + g, (gi_ / kGradSlots) & 1);
-          if (act) {
-            const uint4 x = *reinterpret_cast<const uint4 *>(grad + (size_t)g * kChunk + tid * kVec);
-            float g8[8];
-            unpack_bf16x8(x, g8);
-            if (j == ja) {
+          const uint16_t *gs = grad + (size_t)g * kChunk + tid * 4;
+          const uint2 xa = *reinterpret_cast<const uint2 *>(gs);
+          const uint2 xb = *reinterpret_cast<const uint2 *>(gs + H);
+          float g8[8];
+          unpack_bf16x8(make_uint4(xa.x, xa.y, xb.x, xb.y), g8);
+          if (j == ja) {
 #pragma unroll
-              for (int i = 0; i < 8; ++i) part[i] = g8[i];
-            } else {
+            for (int i = 0; i < 8; ++i) part[i] = g8[i];
+          } else {
 #pragma unroll
-              for (int i = 0; i < 8; ++i) part[i] = __fadd_rn(part[i], g8[i]);
-            }
+            for (int i = 0; i < 8; ++i) part[i] = __fadd_rn(part[i], g8[i]);
           }
           release_slot(gr_empty + g, lane);
           ++gi_;
         }
       }
-      if (act) {  // fold GPU h's partial into the total
-        if (have_tot) {
+      if (have_tot) {  // fold GPU h's partial into the total
 #pragma unroll
-          for (int i = 0; i < 8; ++i) tot[i] = __fadd_rn(tot[i], part[i]);
-        } else {
+        for (int i = 0; i < 8; ++i) tot[i] = __fadd_rn(tot[i], part[i]);
+      } else {
 #pragma unroll
-          for (int i = 0; i < 8; ++i) tot[i] = part[i];
-        }
+        for (int i = 0; i < 8; ++i) tot[i] = part[i];
       }
       have_tot = true;
       ja = jb;
     }
-    if (!act) continue;
+    if (!act_a) continue;  // (act_b implies act_a)
     uint4 wb;
     adam8(a, tot, a.scale[e], w, m, v, wb);                              // a4
     const int64_t so = (int64_t)e * a.spitch + loc - a.s_off;
@@ -522,12 +543,15 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_update_tma(const __grid_cons
     float4 *pm = reinterpret_cast<float4 *>(a.mom1[o] + so);
     float4 *pv = reinterpret_cast<float4 *>(a.mom2[o] + so);
     pw[0] = make_float4(w[0], w[1], w[2], w[3]);
-    pw[1] = make_float4(w[4], w[5], w[6], w[7]);
     pm[0] = make_float4(m[0], m[1], m[2], m[3]);
-    pm[1] = make_float4(m[4], m[5], m[6], m[7]);
     pv[0] = make_float4(v[0], v[1], v[2], v[3]);
-    pv[1] = make_float4(v[4], v[5], v[6], v[7]);
-    place_to(a, e, o, (int64_t)o * a.Pg + loc, wb);                       // a5
+    if (act_b) {
+      pw[H / 4] = make_float4(w[4], w[5], w[6], w[7]);
+      pm[H / 4] = make_float4(m[4], m[5], m[6], m[7]);
+      pv[H / 4] = make_float4(v[4], v[5], v[6], v[7]);
+    }
+    place_split(a, e, o, (int64_t)o * a.Pg + loc, make_uint2(wb.x, wb.y), make_uint2(wb.z, wb.w),
+                act_b);                                                    // a5
   }
 
   // Barrier-out (real mode): "every push into every GPU's slots has landed".  Each consumer
@@ -820,7 +844,6 @@ int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *pl
   }
   a.item_ctr = ctx->item_ctr;
   const bool multi = ctx->rank >= 0 && ctx->G > 1;
-  const uint32_t epoch = ++ctx->upd_epoch;
   const bool dedup = ctx->dedup && !place_only;
   const bool tma = !place_only && (ctx->update_kernel != 0 || dedup);  // de-dup needs the TMA kernel
   a.dedup = dedup ? 1 : 0;
@@ -845,6 +868,9 @@ int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *pl
     }
     ctx->presum_ready = false;
   }
+  // the barrier epoch advances only once every check that can reject the call has passed: a
+  // rank that returned early must not run one epoch ahead of its peers
+  const uint32_t epoch = ++ctx->upd_epoch;
   a.fused_barrier = (multi && tma) ? 1 : 0;  // k_update_tma carries both barriers itself
   a.rank = ctx->rank;
   a.epoch = epoch;

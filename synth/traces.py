@@ -32,6 +32,52 @@ def _softmax_rows(x: np.ndarray) -> np.ndarray:
     return (ex / ex.sum(axis=1, keepdims=True)).astype(np.float32)
 
 
+def _walk_lambda(E: int, it: int, seed: int, sd0: float, step_sd: float, swap_every: int):
+    """Latent log-popularity of iteration `it` and that iteration's generator, positioned after
+    its lambda draws (the token draws come next).  Iteration i's lambda step is the first thing
+    drawn from _rng(seed, i + 1), so replaying those draws gives every iteration independently."""
+    lam = _rng(seed, 0).normal(0.0, sd0, E)
+    rng = _rng(seed, 1)
+    for i in range(1, it + 1):
+        rng = _rng(seed, i + 1)
+        lam = lam + step_sd * rng.normal(size=E)
+        if i % swap_every == 0 and E > 1:
+            hi = int(np.argmax(lam))
+            bottom = np.argsort(lam, kind="stable")[: max(1, E // 2)]
+            j = int(bottom[rng.integers(0, bottom.size)])
+            lam[hi], lam[j] = lam[j], lam[hi]
+    return lam, rng
+
+
+def _walk_tokens(lam, rng, T: int, k: int, chunk: int):
+    E = lam.size
+    ids = np.empty((T, k), dtype=np.int32)
+    gates = np.empty((T, k), dtype=np.float32)
+    for t0 in range(0, T, chunk):
+        t1 = min(T, t0 + chunk)
+        sc = lam[None, :] + rng.gumbel(size=(t1 - t0, E))
+        if k < E:
+            part = np.argpartition(-sc, k - 1, axis=1)[:, :k]
+        else:
+            part = np.tile(np.arange(E), (t1 - t0, 1))
+        psc = np.take_along_axis(sc, part, axis=1)
+        order = np.argsort(-psc, axis=1, kind="stable")
+        sel = np.take_along_axis(part, order, axis=1)
+        ssc = np.take_along_axis(psc, order, axis=1)
+        ids[t0:t1] = sel
+        gates[t0:t1] = _softmax_rows(ssc)
+    return ids, gates
+
+
+def walk_spike_iter(E: int, T: int, k: int, it: int, seed: int, sd0: float = 1.5,
+                    step_sd: float = 0.25, swap_every: int = 3, chunk: int = 32768):
+    """Iteration `it` of ``walk_spike`` alone (identical arrays)."""
+    if not (1 <= k <= E):
+        raise ValueError("need 1 <= k <= E")
+    lam, rng = _walk_lambda(E, it, seed, sd0, step_sd, swap_every)
+    return _walk_tokens(lam, rng, T, k, chunk)
+
+
 def walk_spike(E: int, T: int, k: int, iters: int, seed: int, sd0: float = 1.5,
                step_sd: float = 0.25, swap_every: int = 3, chunk: int = 32768):
     if not (1 <= k <= E):
@@ -47,59 +93,61 @@ def walk_spike(E: int, T: int, k: int, iters: int, seed: int, sd0: float = 1.5,
                 bottom = np.argsort(lam, kind="stable")[: max(1, E // 2)]
                 j = int(bottom[rng.integers(0, bottom.size)])
                 lam[hi], lam[j] = lam[j], lam[hi]
-        ids = np.empty((T, k), dtype=np.int32)
-        gates = np.empty((T, k), dtype=np.float32)
-        for t0 in range(0, T, chunk):
-            t1 = min(T, t0 + chunk)
-            sc = lam[None, :] + rng.gumbel(size=(t1 - t0, E))
-            if k < E:
-                part = np.argpartition(-sc, k - 1, axis=1)[:, :k]
-            else:
-                part = np.tile(np.arange(E), (t1 - t0, 1))
-            psc = np.take_along_axis(sc, part, axis=1)
-            order = np.argsort(-psc, axis=1, kind="stable")
-            sel = np.take_along_axis(part, order, axis=1)
-            ssc = np.take_along_axis(psc, order, axis=1)
-            ids[t0:t1] = sel
-            gates[t0:t1] = _softmax_rows(ssc)
-        out.append((ids, gates))
+        out.append(_walk_tokens(lam, rng, T, k, chunk))
     return out
 
 
-def rotating_hot(E: int, T: int, k: int, iters: int, seed: int, hot_weight: int = 16,
-                 period: int = 3):
+def rotating_hot_iter(E: int, T: int, k: int, it: int, seed: int, hot_weight: int = 16,
+                      period: int = 3):
     if not (1 <= k <= E):
         raise ValueError("need 1 <= k <= E")
     H = max(1, E // 8)
     pairs = T * k
-    out = []
-    for it in range(iters):
-        rng = _rng(seed, it + 1)
-        w = np.ones(E, dtype=np.int64)
-        hot = [((it // period) * H + i) % E for i in range(H)]
-        w[hot] = hot_weight
-        W = int(w.sum())
-        quota = (pairs * w) // W
-        short = pairs - int(quota.sum())
-        quota[:short] += 1  # remainder to the lowest indices (input recipe, not Alg. 1)
-        if int(quota.max()) > T:
-            raise ValueError("quota exceeds T: tokens could not hold distinct experts")
-        fill = np.repeat(np.arange(E, dtype=np.int32), quota)
-        ids = fill.reshape(k, T).T.copy()          # token t gets fill[t], fill[T+t], ...
-        ids = ids[rng.permutation(T)]
-        cols = np.argsort(rng.random((T, k)), axis=1)
-        ids = np.take_along_axis(ids, cols, axis=1).astype(np.int32)
-        gates = _softmax_rows(rng.normal(size=(T, k)))
-        out.append((ids, gates))
-    return out
+    rng = _rng(seed, it + 1)
+    w = np.ones(E, dtype=np.int64)
+    hot = [((it // period) * H + i) % E for i in range(H)]
+    w[hot] = hot_weight
+    W = int(w.sum())
+    quota = (pairs * w) // W
+    short = pairs - int(quota.sum())
+    quota[:short] += 1  # remainder to the lowest indices (input recipe, not Alg. 1)
+    if int(quota.max()) > T:
+        raise ValueError("quota exceeds T: tokens could not hold distinct experts")
+    fill = np.repeat(np.arange(E, dtype=np.int32), quota)
+    ids = fill.reshape(k, T).T.copy()          # token t gets fill[t], fill[T+t], ...
+    ids = ids[rng.permutation(T)]
+    cols = np.argsort(rng.random((T, k)), axis=1)
+    ids = np.take_along_axis(ids, cols, axis=1).astype(np.int32)
+    gates = _softmax_rows(rng.normal(size=(T, k)))
+    return ids, gates
 
 
-def make_trace(workload, iters: int | None = None, seed: int | None = None, T: int | None = None):
-    """Trace for a ``synth.configs.Workload``; T may be overridden (bounded samples)."""
+def rotating_hot(E: int, T: int, k: int, iters: int, seed: int, hot_weight: int = 16,
+                 period: int = 3):
+    return [rotating_hot_iter(E, T, k, it, seed, hot_weight, period) for it in range(iters)]
+
+
+def _trace_iter(args):
+    kind, E, T, k, it, sd = args
+    if kind == "rotating-hot":
+        return rotating_hot_iter(E, T, k, it, sd)
+    return walk_spike_iter(E, T, k, it, sd)
+
+
+def make_trace(workload, iters: int | None = None, seed: int | None = None, T: int | None = None,
+               workers: int = 1):
+    """Trace for a ``synth.configs.Workload``; T may be overridden (bounded samples).  With
+    workers > 1 the iterations are generated in a process pool (identical arrays: every
+    iteration is computed independently)."""
     from .configs import seed_for
     it = workload.iters if iters is None else iters
     sd = seed_for(workload.name) if seed is None else seed
     TT = workload.T if T is None else T
+    jobs = [(workload.trace, workload.E, TT, workload.k, i, sd) for i in range(it)]
+    if workers > 1 and it > 1:
+        import multiprocessing as mp
+        with mp.get_context("fork").Pool(min(workers, it)) as pool:
+            return pool.map(_trace_iter, jobs)
     if workload.trace == "rotating-hot":
         return rotating_hot(workload.E, TT, workload.k, it, sd)
     return walk_spike(workload.E, TT, workload.k, it, sd)

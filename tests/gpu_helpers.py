@@ -6,21 +6,39 @@ import numpy as np
 import torch
 
 from oracle import step as ostep
-from synth import configs, hashgen, traces
+from synth import configs, edge, hashgen, traces
 
 
 def _u32(x: np.ndarray) -> np.ndarray:
     return np.ascontiguousarray(x).view(np.uint32)
 
 
+def _state_equal(got: np.ndarray, want: np.ndarray) -> bool:
+    """fp32 state parity.  Every non-NaN element bitwise; NaN policy (A22): a NaN
+    on one side must be a NaN on the other, payload and sign not compared (the GPU produces the
+    canonical 0x7FFFFFFF, x86 the default 0xFFC00000 or the first operand's payload)."""
+    got = np.ascontiguousarray(got, dtype=np.float32)
+    want = np.ascontiguousarray(want, dtype=np.float32)
+    ng, nw = np.isnan(got), np.isnan(want)
+    if not np.array_equal(ng, nw):
+        return False
+    return np.array_equal(_u32(got)[~ng], _u32(want)[~nw])
+
+
 def run_parity(name: str, G: int, iters: int, *, rank_mode: str = "virtual", idx=None,
                T: int | None = None, policy: int = 0, scale_mode: int = 0, scale=None,
                weight_decay: float = 0.0, trace=None, check_dispatch: bool = True,
                dedup: bool = False, capacity: int = 0, replan_interval: int = 1,
-               host_state: bool = False, lazy_replicate: bool = False, seed: int | None = None):
+               host_state: bool = False, lazy_replicate: bool = False, seed: int | None = None,
+               grads: str = "hash", masters: str = "hash", zero_idle: bool = False):
     """Returns the number of iterations compared.  rank_mode: "virtual" (rank=-1, G ranks on
     cuda:0) or "single" (real mode with G == 1).  `name` is a config name or an ad-hoc
-    synth.configs.Workload (then pass `seed`)."""
+    synth.configs.Workload (then pass `seed`).
+
+    Update-stage edge values (synth/edge.py): grads="edge" / masters="edge" draw +-0,
+    denormals, overflow-range values, +-inf and NaN; zero_idle=True gives every slot of an
+    expert that received no pair in the iteration an exactly-zero gradient (the backward of
+    an expert no token flowed through)."""
     from paper_2504_19925_b200 import AdamConfig, DecoupledExpertLayer
     from paper_2504_19925_b200.api import synth_grads
     from oracle.adam import AdamHyper
@@ -41,25 +59,53 @@ def run_parity(name: str, G: int, iters: int, *, rank_mode: str = "virtual", idx
     layer = DecoupledExpertLayer(E, G, S, k, P, Tg, rank=rank, device=0, seed=seed, adam=adam,
                                  policy=policy, scale_mode=scale_mode, scale=scale, dedup=dedup,
                                  capacity=capacity, replan_interval=replan_interval,
-                                 host_state=host_state, lazy_replicate=lazy_replicate)
+                                 host_state=host_state, lazy_replicate=lazy_replicate,
+                                 init_master=(masters == "hash"))
     pol = {0: "alg1", 1: "minmax", 2: "static"}[policy]
     idx_arr = np.arange(P, dtype=np.int64) if idx is None else np.asarray(idx, dtype=np.int64)
+    Pg = P // G
+    master0 = None
+    if masters == "edge":
+        from paper_2504_19925_b200 import api
+        for v in range(layer.n_local):
+            owner = v if rank < 0 else rank
+            loc = np.arange(owner * Pg, (owner + 1) * Pg, dtype=np.uint64)
+            bits = np.stack([edge.edge_master_bits(seed, e, loc) for e in range(E)])
+            layer.master[v].copy_(torch.from_numpy(bits.view(np.float32).reshape(-1)))
+        api.moe_place(layer.ctx, layer.plan)
+        master0 = np.stack([edge.edge_master_bits(seed, e, idx_arr.astype(np.uint64))
+                            for e in range(E)]).view(np.float32)
     sim = ostep.OracleSim(E, G, S, P, seed, hyper=hyper, policy=pol, scale_mode=scale_mode,
                           scale=scale, idx=idx_arr, capacity=capacity,
-                          replan_interval=replan_interval)
+                          replan_interval=replan_interval, master0=master0)
     idx_t = torch.from_numpy(idx_arr).cuda()
-    Pg = P // G
+    gen = edge.edge_grad_bits if grads == "edge" else hashgen.grad_bits
     # initial placement (moe_place) equals the oracle's plan_0 placement
     _compare_weights(layer, sim, idx_t, G, S, P)
     tr = trace if trace is not None else traces.make_trace(wl, iters=iters, T=TT, seed=seed)
     for t, (ids, gates) in enumerate(tr[:iters]):
+        # slots of experts with no pair this iteration (under plan_t, the oracle's) get zeros
+        zs = set(edge.zero_slots(ids, E, sim.plan["slot_expert"]).tolist()) if zero_idle else set()
         for v in range(layer.n_local):
-            synth_grads(layer.slot_g[v], seed, t, v * S, S, P)
+            if grads == "edge":
+                full = np.arange(P, dtype=np.uint64)
+                bits = np.stack([gen(seed, t, j, full) for j in range(v * S, (v + 1) * S)])
+                layer.slot_g[v].view(torch.int16).copy_(torch.from_numpy(bits.view(np.int16).reshape(-1)))
+            else:
+                synth_grads(layer.slot_g[v], seed, t, v * S, S, P)
+            for j in sorted(zs):
+                if v * S <= j < (v + 1) * S:
+                    layer.slot_g[v][(j - v * S) * P:(j - v * S + 1) * P].zero_()
         ids_d = torch.from_numpy(np.ascontiguousarray(ids)).cuda()
         gates_d = torch.from_numpy(np.ascontiguousarray(gates)).cuda()
         layer.iterate(ids_d, gates_d, Tg)
-        res = sim.iterate(traces.split_ranks(ids, G), traces.split_ranks(gates, G),
-                          lambda j, t=t: hashgen.grad_bits(seed, t, j, idx_arr.astype(np.uint64)))
+
+        def grad_of_slot(j, t=t):
+            if j in zs:
+                return np.zeros(idx_arr.size, dtype=np.uint16)
+            return gen(seed, t, j, idx_arr.astype(np.uint64))
+        with np.errstate(all="ignore"):      # edge values overflow / make NaN on purpose
+            res = sim.iterate(traces.split_ranks(ids, G), traces.split_ranks(gates, G), grad_of_slot)
         layer.ctx.check()
         pn = res["plan_next"]
         assert layer.plan.replicas.tolist() == pn["replicas"].tolist(), f"iter {t}: replicas"
@@ -97,7 +143,7 @@ def run_parity(name: str, G: int, iters: int, *, rank_mode: str = "virtual", idx
             for name_, arr, want in (("master", layer.master, sim.master), ("m", layer.adam_m, sim.m),
                                      ("v", layer.adam_v, sim.v)):
                 got = arr[v].view(E, Pg)[:, li.to(arr[v].device)].cpu().numpy()
-                assert np.array_equal(_u32(got), _u32(want[:, cols])), f"iter {t} owner {v}: {name_}"
+                assert _state_equal(got, want[:, cols]), f"iter {t} owner {v}: {name_}"
         _compare_weights(layer, sim, idx_t, G, S, P, t)
     layer.close()
     return iters

@@ -312,3 +312,42 @@ def test_random_small_configs_fuzz(case):
                lazy_replicate=dedup and rng.random() < 0.5, host_state=rng.random() < 0.2,
                scale_mode=scale_mode, scale=scale,
                weight_decay=0.01 if rng.random() < 0.3 else 0.0)
+
+
+@pytest.mark.parametrize("name,G,dedup,kernel,host_state", [
+    ("tiny-skew", 1, False, "tma", False), ("tiny-skew", 4, True, "tma", False),
+    ("tiny-odd", 3, False, "tma", False), ("medium", 1, False, "tma", False),
+    ("medium", 4, True, "tma", False), ("medium", 4, False, "ldg", False),
+    ("tiny-skew", 4, True, "tma", True), ("tiny-odd", 3, False, "ldg", True)])
+def test_update_edge_values(name, G, dedup, kernel, host_state, monkeypatch):
+    """Update-stage edge values through the whole step, every element, every iteration
+    (synth/edge.py): a routing where a changing set of experts gets no token (down to k
+    active experts) and every slot of such an expert carries an exactly-zero gradient
+    (every expert keeps >= 1 replica; its optimizer
+    still steps); the other slots carry +-0, bf16 denormals, values whose square overflows
+    (v = +inf, step 0), values whose replica sum overflows, +-inf and NaN; masters +-0,
+    denormal, bf16 rounding ties and values whose RNE to bf16 overflows.  fp32 state bitwise
+    except NaN (mask compared, reading A22); bf16 weights bitwise (NaN -> 0x7FFF, A17).
+    Both update kernels, HBM- and host-resident state, with and without de-dup."""
+    from gpu_helpers import run_parity
+    from synth import edge
+    if kernel == "ldg":
+        monkeypatch.setenv("MOE_UPDATE_KERNEL", "ldg")
+    wl = configs.CONFIGS[name]
+    tr = edge.idle_expert_trace(wl.E, wl.T, wl.k, 6, seed=configs.seed_for(name))
+    mode = "single" if G == 1 else "virtual"
+    run_parity(name, G, 6, trace=tr, grads="edge", masters="edge", zero_idle=True, dedup=dedup,
+               rank_mode=mode, host_state=host_state)
+
+
+@pytest.mark.parametrize("name,G,dedup", [("tiny-skew", 4, True), ("medium", 1, False), ("medium", 4, True)])
+def test_zero_token_experts_step_with_zero_grads(name, G, dedup):
+    """Experts that receive no token keep their replica (Alg. 1's min-1 clamp) and step
+    their optimizer on an exactly-zero reduced gradient (m, v decay; w moves by the decayed
+    momentum) -- the normal-range grads everywhere else; bitwise vs the oracle."""
+    from gpu_helpers import run_parity
+    from synth import edge
+    wl = configs.CONFIGS[name]
+    tr = edge.idle_expert_trace(wl.E, wl.T, wl.k, 6, seed=11)
+    run_parity(name, G, 6, trace=tr, zero_idle=True, dedup=dedup,
+               rank_mode="single" if G == 1 else "virtual")

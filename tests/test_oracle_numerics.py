@@ -156,6 +156,54 @@ def test_adam_matches_torch_optim(wd):
     assert np.max(np.abs(v - tv)) <= 1e-6 * np.max(np.abs(tv))
 
 
+def test_adam_edge_values_match_torch_optim():
+    """Update-stage edge values (synth/edge.py: +-0, denormals, g*g overflow, sums past the
+    bf16 range, +-inf, NaN; masters +-0, denormal, near FLT_MAX) over 8 steps against
+    torch.optim.Adam (foreach=False, fused=False; independent code, lerp for m): the same
+    NaN positions, the same infinities, and every finite weight within 1e-6 of the
+    parameter's scale (at least the 8 steps' lr, for weights that start at +-0) plus 4 denormal ulps (denormal results carry absolute, not relative,
+    precision).  Finite grads of magnitude >= 2^127 are replaced by +-2^120 here only: torch's
+    lerp form m + 0.1 (g - m) overflows on g - m where the paper-order 0.9 m + 0.1 g does not."""
+    from synth import edge
+    h = A.AdamHyper(lr=1e-3)
+    n = 1 << 15
+    idx = np.arange(n, dtype=np.uint64)
+    w0 = edge.edge_master_bits(21, 3, idx).view(np.float32).copy()
+    p = torch.nn.Parameter(torch.from_numpy(w0.copy()))
+    opt = torch.optim.Adam([p], lr=h.lr, betas=(h.beta1, h.beta2), eps=h.eps, foreach=False,
+                           fused=False)
+    w, m, v = w0.copy(), np.zeros(n, np.float32), np.zeros(n, np.float32)
+    with np.errstate(all="ignore"):
+        for t in range(1, 9):
+            g = N.bf16_to_f32(edge.edge_grad_bits(21, t, 0, idx))
+            g = np.where(np.isfinite(g) & (np.abs(g) >= 2.0 ** 127), np.sign(g) * 2.0 ** 120, g).astype(np.float32)
+            p.grad = torch.from_numpy(g.copy())
+            opt.step()
+            w, m, v = A.adam_update(w, m, v, g, A.scalars(h, t))
+        tw = p.detach().numpy()
+        assert np.array_equal(np.isnan(w), np.isnan(tw))
+        assert np.isnan(w).any() and np.isinf(v).any() and (v == 0).any()   # cases exercised
+        fin = np.isfinite(tw)
+        assert np.array_equal(np.isinf(w), np.isinf(tw)) and np.array_equal(w[~fin & ~np.isnan(tw)],
+                                                                            tw[~fin & ~np.isnan(tw)])
+        tol = 1e-6 * np.maximum(np.maximum(np.abs(tw[fin]), np.abs(w0[fin])), 8 * h.lr).astype(np.float64) + 4 * 2.0 ** -149
+        assert (np.abs(w[fin].astype(np.float64) - tw[fin]) <= tol).all()
+
+
+def test_adam_overflowing_square_freezes_weight():
+    """|g| >= 2^73 at t = 1: v = (1-b2) g*g overflows to +inf, den = +inf, the step m/den is
+    exactly 0 (m finite), so w keeps its bits; m = fp32(0.1 * g) by the closed form."""
+    h = A.AdamHyper()
+    g = np.array([2.0 ** 73, -2.0 ** 100, 2.0 ** 120 * 1.5], dtype=np.float32)
+    w0 = np.array([0.5, -1e-40, 3.0e38], dtype=np.float32)
+    z = np.zeros_like(w0)
+    with np.errstate(over="ignore"):
+        w1, m1, v1 = A.adam_update(w0, z, z, g, A.scalars(h, 1))
+    assert np.isposinf(v1).all()
+    assert np.array_equal(w1.view(np.uint32), w0.view(np.uint32))
+    assert np.array_equal(m1, np.array([np.float32(np.float32(0.1) * x) for x in g.tolist()], np.float32))
+
+
 def test_sharded_adam_equals_unsharded():
     h = A.AdamHyper()
     n, G = 4096, 4
