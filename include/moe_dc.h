@@ -56,7 +56,7 @@
 extern "C" {
 #endif
 
-#define MOE_ABI_VERSION 5
+#define MOE_ABI_VERSION 6
 #define MOE_MAX_E 256     /* experts per layer                              */
 #define MOE_MAX_G 8       /* GPUs: one NVSwitch box                         */
 #define MOE_MAX_SLOTS 4096 /* G*S                                           */
@@ -80,6 +80,10 @@ typedef enum {
 const char *moe_status_str(int status);
 const char *moe_last_error(void);
 int moe_abi_version(void);
+/* Build provenance: 16 hex digits of sha256 over the sources, headers, compiler flags and
+ * nvcc version this library was built from (paper_2504_19925_b200/_build.py source_hash).
+ * Static storage; never NULL.                                                            */
+const char *moe_build_id(void);
 
 /* ------------------------------------------------------------------------------------------
  * a1 Plan -- host only, synchronous, pure, thread-safe; no CUDA.
@@ -103,8 +107,11 @@ typedef enum {
   MOE_PLAN_STATIC = 2,     /* row f2, reading B2: the static baseline's uniform replication,
                               r_e = G*S/E (remainder to the lowest indices); counts ignored
                               ("an equal number of expert instances")          */
-  MOE_PLAN_KEEP = 3        /* moe_step only (row f2, reading B3 interval policy): plan_next =
+  MOE_PLAN_KEEP = 3,       /* moe_step only (row f2, reading B3 interval policy): plan_next =
                               plan_cur, i.e. no re-placement this iteration                  */
+  MOE_PLAN_SCHEDULED = 4   /* moe_step only: the context's schedule (moe_ctx_set_schedule)
+                              decides, for the step's Adam counter t, between re-placing and
+                              keeping (moe_plan_scheduled)                                    */
 } moe_plan_policy;
 
 /* counts: [E] global pair counts C_e >= 0 (host).  sum == 0 means uniform (reading A3).
@@ -117,6 +124,19 @@ int moe_plan(const int64_t *counts, int32_t E, int32_t G, int32_t slots, moe_pla
  * tokens / (s N) per slot): max(1, floor(cf * T * k / (G * S))), T global tokens
  * (tokens counted as (token, expert) pairs, reading A6).  Returns -1 on invalid input.      */
 int32_t moe_slot_capacity(double cf, int64_t T, int32_t k, int32_t G, int32_t S);
+
+/* Row f2 (reading B3, "every i = 10, 50, or 100 iterations"): the
+ * placement scheduler's decision for the iteration whose Adam step counter is `step` (>= 1).
+ * With replan_interval i >= 1 it re-places with `policy` (ALG1, MINMAX or STATIC) from this
+ * iteration's counts after every iteration with step % i == 0 -- i = 1 is the paper's design,
+ * re-placement every iteration -- and otherwise keeps the placement: plan_next = plan_cur.
+ * plan_cur must be a valid placement (E, G, S, arrays); plan_next's arrays are written.
+ * replanned (nullable) receives 1 if the call re-placed, else 0.
+ * Errors: MOE_ERR_INVALID (NULL pointer, step < 1, replan_interval < 1, bad policy, the
+ * moe_plan_ex errors), MOE_ERR_SHAPE (plan_cur not a valid contiguous placement).          */
+int moe_plan_scheduled(const int64_t *counts, const moe_plan_t *plan_cur, int32_t policy,
+                       int32_t replan_interval, int64_t step, moe_plan_t *plan_next,
+                       int32_t *replanned);
 
 /* As moe_plan with an explicit policy.  steps (nullable, [2]) receives the number of
  * over- and under-allocation correction steps of Alg. 1 (0 for MINMAX).           */
@@ -225,6 +245,11 @@ int moe_ctx_get_timing(moe_ctx *ctx, double *dispatch_ms, int64_t *n_dispatch, d
 #define MOE_TIMING_STAGES 8
 int moe_ctx_get_timing_ex(moe_ctx *ctx, double *ms, int64_t *n);
 
+/* The schedule moe_step(..., MOE_PLAN_SCHEDULED, ...) follows (moe_plan_scheduled with the
+ * step's adam->step).  Default at creation: MOE_PLAN_PAPER_ALG1, replan_interval 1.
+ * Errors: MOE_ERR_INVALID (NULL ctx, policy not ALG1/MINMAX/STATIC, replan_interval < 1).    */
+int moe_ctx_set_schedule(moe_ctx *ctx, int32_t policy, int32_t replan_interval);
+
 /* Synchronises `stream`, then reports and clears device-raised errors
  * (MOE_ERR_DATA, MOE_ERR_TIMEOUT).                                               */
 int moe_ctx_check(moe_ctx *ctx, void *stream);
@@ -329,7 +354,9 @@ int moe_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *plan_
  * Scheduling inside: with MOE_OPT_DEDUP the local partial sums start first on a library side
  * stream; the three dispatch kernels run on a highest-priority library stream; both are
  * joined to `stream` by events, so the caller sees ordinary stream semantics.
- * policy: a moe_plan_policy (MOE_PLAN_KEEP = keep plan_cur, the interval policy).
+ * policy: a moe_plan_policy -- MOE_PLAN_SCHEDULED follows the context's schedule
+ * (moe_ctx_set_schedule; the library decides re-place vs keep from adam->step), MOE_PLAN_KEEP
+ * keeps plan_cur, ALG1 / MINMAX / STATIC re-place unconditionally.
  * Errors: those of the four calls; MOE_ERR_INVALID if out->counts_host is NULL.           */
 int moe_step(moe_ctx *ctx, const int32_t *topk_ids, const float *gates, int64_t T,
              const moe_plan_t *plan_cur, moe_plan_t *plan_next, int32_t policy,

@@ -7,7 +7,7 @@ one MoE layer's iteration.  There is no CPU fallback: importing ``api`` without 
 library raises.
 """
 from .api import (AdamConfig, DispatchBuffers, MoeContext, MoeError, Plan,  # noqa: F401
-                  MOE_OPT_DEDUP, MOE_OPT_HOST_STATE, MOE_OPT_LAZY_REPLICATE, MOE_PLAN_KEEP, MOE_PLAN_MINMAX, MOE_PLAN_PAPER_ALG1,
+                  MOE_OPT_DEDUP, MOE_OPT_HOST_STATE, MOE_OPT_LAZY_REPLICATE, MOE_PLAN_KEEP, MOE_PLAN_MINMAX, MOE_PLAN_SCHEDULED, MOE_PLAN_PAPER_ALG1,
                   MOE_PLAN_STATIC, moe_dispatch, moe_place, moe_plan, moe_slot_capacity, moe_step,
                   moe_update, synth_grads, synth_master, TokenExchange, MOE_TOK_GATE,
                   moe_token_dispatch, moe_token_combine)

@@ -36,11 +36,32 @@ CXXFLAGS = ["-O2", "-fPIC", "-std=c++17", "-ffp-contract=off", "-fno-fast-math",
             "-I", INC, "-I", CSRC, "-I", "/usr/local/cuda/include"]
 
 
-def _stale(target: str, deps) -> bool:
-    if not os.path.exists(target):
-        return True
-    t = os.path.getmtime(target)
-    return any(os.path.getmtime(d) > t for d in deps)
+def source_hash() -> str:
+    """16 hex digits of sha256 over every source and header this library is built from, the
+    compiler flags and the nvcc version: the build id embedded in libmoedc.so (moe_build_id)."""
+    import hashlib
+    h = hashlib.sha256()
+    for path in [os.path.join(CSRC, f) for f in CU + CPP] + HEADERS:
+        h.update(os.path.basename(path).encode() + b"\0" + open(path, "rb").read() + b"\0")
+    h.update(" ".join(NVFLAGS + CXXFLAGS).replace(ROOT, "<root>").encode())
+    try:
+        h.update(subprocess.run([NVCC, "--version"], capture_output=True, text=True).stdout.encode())
+    except OSError:
+        pass
+    return h.hexdigest()[:16]
+
+
+MARK = b"MOEDC_BUILD_ID="
+
+
+def built_id(path: str = OUT) -> str | None:
+    """The build id embedded in an existing libmoedc.so (read from the file, not loaded)."""
+    try:
+        data = open(path, "rb").read()
+    except OSError:
+        return None
+    i = data.find(MARK)
+    return data[i + len(MARK):i + len(MARK) + 16].decode("ascii", "replace") if i >= 0 else None
 
 
 def _run(cmd, verbose):
@@ -55,23 +76,31 @@ def _run(cmd, verbose):
 
 
 def build(verbose: bool = False, ptxas_verbose: bool = False) -> str:
+    """Rebuilds everything unless the in-tree libmoedc.so carries the build id of the current
+    sources and flags (no mtime trust: a stale binary shipped with the tree is replaced)."""
+    bid = source_hash()
+    if built_id() == bid and not ptxas_verbose:
+        return OUT
     os.makedirs(OBJ, exist_ok=True)
-    objs = []
+    defs = [f"-DMOE_BUILD_ID=\"{bid}\""]
+    cmds, objs = [], []
     for f in CU:
-        src = os.path.join(CSRC, f)
         obj = os.path.join(OBJ, f + ".o")
-        if _stale(obj, [src] + HEADERS) or ptxas_verbose:
-            extra = ["-Xptxas", "-v"] if ptxas_verbose else []
-            _run([NVCC] + NVFLAGS + extra + ["-c", src, "-o", obj], verbose or ptxas_verbose)
+        extra = ["-Xptxas", "-v"] if ptxas_verbose else []
+        cmds.append([NVCC] + NVFLAGS + defs + extra + ["-c", os.path.join(CSRC, f), "-o", obj])
         objs.append(obj)
     for f in CPP:
-        src = os.path.join(CSRC, f)
         obj = os.path.join(OBJ, f + ".o")
-        if _stale(obj, [src] + HEADERS):
-            _run(["g++"] + CXXFLAGS + ["-c", src, "-o", obj], verbose)
+        cmds.append(["g++"] + CXXFLAGS + defs + ["-c", os.path.join(CSRC, f), "-o", obj])
         objs.append(obj)
-    if _stale(OUT, objs):
-        _run([NVCC] + ARCH + ["-shared", "-o", OUT] + objs, verbose)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 1)) as ex:
+        list(ex.map(lambda c: _run(c, verbose or ptxas_verbose), cmds))
+    tmp = OUT + ".tmp"
+    _run([NVCC] + ARCH + ["-shared", "-o", tmp] + objs, verbose)
+    os.replace(tmp, OUT)
+    if built_id() != bid:
+        raise RuntimeError("libmoedc.so does not carry the expected build id")
     return OUT
 
 

@@ -15,12 +15,12 @@ MOE_OK = 0
 STATUS = {0: "MOE_OK", 1: "MOE_ERR_INVALID", 2: "MOE_ERR_SHAPE", 3: "MOE_ERR_DATA",
           4: "MOE_ERR_CUDA", 5: "MOE_ERR_COMM", 6: "MOE_ERR_INTERNAL", 7: "MOE_ERR_TIMEOUT"}
 MOE_MAX_E, MOE_MAX_G, MOE_MAX_SLOTS = 256, 8, 4096
-MOE_PLAN_PAPER_ALG1, MOE_PLAN_MINMAX, MOE_PLAN_STATIC, MOE_PLAN_KEEP = 0, 1, 2, 3
+MOE_PLAN_PAPER_ALG1, MOE_PLAN_MINMAX, MOE_PLAN_STATIC, MOE_PLAN_KEEP, MOE_PLAN_SCHEDULED = 0, 1, 2, 3, 4
 
 # every symbol include/*.h declares (checked by tests/test_abi.py)
 EXPORTED = [
-    "moe_status_str", "moe_last_error", "moe_abi_version", "moe_plan", "moe_plan_ex",
-    "moe_slot_capacity",
+    "moe_status_str", "moe_last_error", "moe_abi_version", "moe_build_id", "moe_plan", "moe_plan_ex",
+    "moe_slot_capacity", "moe_plan_scheduled", "moe_ctx_set_schedule",
     "moe_ctx_create", "moe_ctx_destroy", "moe_ctx_handle_bytes", "moe_ctx_export",
     "moe_ctx_connect", "moe_ctx_check", "moe_ctx_wait_counts", "moe_ctx_weights_wait", "moe_dispatch", "moe_update",
     "moe_place", "moe_step", "moe_ctx_set_timing", "moe_ctx_get_timing", "moe_ctx_get_timing_ex",
@@ -90,6 +90,13 @@ def lib() -> C.CDLL:
         L.moe_plan_ex.argtypes = [_i64p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                   C.POINTER(MoePlanT), _i64p]
         L.moe_ctx_create.restype = C.c_int
+        L.moe_build_id.restype = C.c_char_p
+        L.moe_build_id.argtypes = []
+        L.moe_plan_scheduled.restype = C.c_int
+        L.moe_plan_scheduled.argtypes = [_i64p, C.POINTER(MoePlanT), C.c_int32, C.c_int32, C.c_int64,
+                                         C.POINTER(MoePlanT), _i32p]
+        L.moe_ctx_set_schedule.restype = C.c_int
+        L.moe_ctx_set_schedule.argtypes = [C.c_void_p, C.c_int32, C.c_int32]
         L.moe_ctx_create.argtypes = [C.POINTER(MoeCtxDesc), C.POINTER(C.c_void_p)]
         L.moe_ctx_destroy.restype = C.c_int
         L.moe_ctx_destroy.argtypes = [C.c_void_p]

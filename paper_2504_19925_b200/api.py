@@ -14,7 +14,7 @@ import torch
 
 from . import _lib as L
 from ._lib import (MOE_OPT_DEDUP, MOE_OPT_HOST_STATE, MOE_OPT_LAZY_REPLICATE, MOE_PLAN_KEEP, MOE_PLAN_MINMAX, MOE_PLAN_PAPER_ALG1,  # noqa: F401
-                   MOE_PLAN_STATIC, MoeError, check)
+                   MOE_PLAN_SCHEDULED, MOE_PLAN_STATIC, MoeError, check)
 
 
 def _stream_ptr(stream) -> C.c_void_p:
@@ -44,16 +44,6 @@ class Plan:
     def c(self) -> L.MoePlanT:
         return self._c
 
-    @classmethod
-    def from_first_slot(cls, first_slot, G: int, S: int) -> "Plan":
-        fs = np.asarray(first_slot, dtype=np.int32)
-        p = cls(fs.size - 1, G, S)
-        p.first_slot[:] = fs
-        p.replicas[:] = np.diff(fs)
-        p.slot_expert[:] = np.repeat(np.arange(p.E, dtype=np.int32), p.replicas)
-        return p
-
-
 def moe_slot_capacity(cf: float, T: int, k: int, G: int, S: int) -> int:
     """Row f2: max(1, floor(cf * T * k / (G * S))) (computed by the C library)."""
     c = L.lib().moe_slot_capacity(cf, T, k, G, S)
@@ -73,6 +63,18 @@ def moe_plan(counts, E: int, G: int, slots: int, policy: int = MOE_PLAN_PAPER_AL
     check(L.lib().moe_plan_ex(c.ctypes.data_as(C.POINTER(C.c_int64)), E, G, slots, policy,
                               C.byref(p.c), steps.ctypes.data_as(C.POINTER(C.c_int64))), "moe_plan")
     return (p, (int(steps[0]), int(steps[1]))) if return_steps else p
+
+
+def moe_plan_scheduled(counts, plan_cur: Plan, policy: int, replan_interval: int, step: int) -> Plan:
+    """a1 under row f2's schedule (host C++): re-place with `policy` when step % interval == 0,
+    else keep plan_cur."""
+    c = np.ascontiguousarray(counts, dtype=np.int64)
+    if c.size != plan_cur.E:
+        raise ValueError("counts must have E entries")
+    p = Plan(plan_cur.E, plan_cur.G, plan_cur.S)
+    check(L.lib().moe_plan_scheduled(c.ctypes.data_as(C.POINTER(C.c_int64)), C.byref(plan_cur.c), policy,
+                                     replan_interval, step, C.byref(p.c), None), "moe_plan_scheduled")
+    return p
 
 
 def gather_records(record: bytes, G: int, group=None) -> list[bytes]:
@@ -156,6 +158,10 @@ class MoeContext:
     def connect_process_group(self, group=None) -> None:
         """Exchange the CUDA-IPC records over a torch.distributed group and map the peers."""
         self.connect(gather_records(self.export(), self.G, group))
+
+    def set_schedule(self, policy: int, replan_interval: int) -> None:
+        """The placement schedule moe_step(MOE_PLAN_SCHEDULED) follows (row f2)."""
+        check(L.lib().moe_ctx_set_schedule(self.handle, policy, replan_interval), "moe_ctx_set_schedule")
 
     def set_timing(self, enable: bool) -> None:
         check(L.lib().moe_ctx_set_timing(self.handle, int(enable)), "moe_ctx_set_timing")

@@ -32,3 +32,4 @@ int moe_step_abort(moe_ctx *ctx, int status);  // forgets an early k_presum; ret
 void *moe_hi_begin(moe_ctx *ctx, void *stream);          // stream for moe_step's dispatch
 int moe_hi_end(moe_ctx *ctx, void *hi, void *stream);    // join it back
 void moe_host_time(moe_ctx *ctx, int which, double ms);  // 0: wait for C_t, 1: planner, 2: launch
+void moe_ctx_schedule(const moe_ctx *ctx, int32_t *policy, int32_t *interval);  // ctx.cu

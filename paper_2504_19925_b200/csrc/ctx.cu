@@ -176,6 +176,8 @@ extern "C" int moe_ctx_create(const moe_ctx_desc *d, moe_ctx **out) {
   c->device = d->device;
   c->connected = false;
   c->disp_epoch = c->upd_epoch = 0;
+  c->sched_policy = MOE_PLAN_PAPER_ALG1;
+  c->sched_interval = 1;
   c->sync = nullptr;
   c->cnt_local = nullptr;
   c->done = nullptr;
@@ -443,6 +445,21 @@ extern "C" int moe_ctx_wait_counts(moe_ctx *ctx) {
   std::atomic_thread_fence(std::memory_order_acquire);
   ctx->counts_pending = false;
   return MOE_OK;
+}
+
+extern "C" int moe_ctx_set_schedule(moe_ctx *ctx, int32_t policy, int32_t replan_interval) {
+  if (!ctx) return fail(MOE_ERR_INVALID, "moe_ctx_set_schedule: NULL ctx");
+  if (policy != MOE_PLAN_PAPER_ALG1 && policy != MOE_PLAN_MINMAX && policy != MOE_PLAN_STATIC)
+    return fail(MOE_ERR_INVALID, "moe_ctx_set_schedule: policy %d is not a placement policy", policy);
+  if (replan_interval < 1) return fail(MOE_ERR_INVALID, "moe_ctx_set_schedule: replan_interval < 1");
+  ctx->sched_policy = policy;
+  ctx->sched_interval = replan_interval;
+  return MOE_OK;
+}
+
+void moe_ctx_schedule(const moe_ctx *ctx, int32_t *policy, int32_t *interval) {
+  *policy = ctx->sched_policy;
+  *interval = ctx->sched_interval;
 }
 
 extern "C" int moe_ctx_set_timing(moe_ctx *ctx, int32_t enable) {

@@ -29,6 +29,12 @@
 namespace moe {
 namespace {
 
+__device__ __forceinline__ uint32_t atom_add_acq_rel_gpu(uint32_t *p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
 struct HistArgs {
   const int32_t *ids;
   int64_t npairs;  // pairs per rank = T*k
@@ -114,17 +120,14 @@ __global__ void __launch_bounds__(kThreads) k_hist(const __grid_constant__ HistA
     blk[(int64_t)e * a.nb_max + b] = h;
     if (h) atomicAdd(a.cnt_local + v * a.E + e, h);
   }
-  // ticket: bar.sync orders the block's writes before thread 0's (cumulative) fence
+  // ticket: bar.sync orders the block's writes before thread 0's acq_rel atomic (release is
+  // cumulative); the last block's acquire makes every block's counts visible to it
   __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    is_last = (atomicAdd(a.done + v, 1u) == (unsigned)(a.nb - 1));
-  }
+  if (tid == 0) is_last = (atom_add_acq_rel_gpu(a.done + v, 1u) == (unsigned)(a.nb - 1));
   __syncthreads();
   if (!is_last) return;
 
   // Last tile of rank v: publish the rank's counts (a0).
-  __threadfence();
   const int grank = a.real ? a.rank : v;
   for (int e = tid; e < a.E; e += kThreads) {
     const int32_t c = atomicExch(a.cnt_local + v * a.E + e, 0);  // read + reset for next call
@@ -141,9 +144,8 @@ __global__ void __launch_bounds__(kThreads) k_hist(const __grid_constant__ HistA
   if (host)
     for (int e = tid; e < a.E; e += kThreads) a.counts_host[e] = a.dst[0]->xcnt[a.parity][grank][e];
   __syncthreads();
-  if (tid == 0) {
-    if (flags || host) __threadfence_system();
-    a.done[v] = 0;
+  if (tid == 0) {  // st.release.sys after bar.sync: orders every thread's count stores before
+    a.done[v] = 0;  // the flag (the CUTLASS semaphore-release pattern, at system scope)
     if (flags)
       for (int h = 0; h < a.G; ++h) st_release_sys(&a.dst[h]->disp_flag[grank], a.epoch);
     if (host) st_release_sys(a.host_flag, a.epoch);
@@ -304,13 +306,9 @@ __global__ void __launch_bounds__(kThreads) k_scan(const __grid_constant__ ScanA
   // dispatch instead of one per expert (it was ~40 % of this kernel's stall samples).
   __shared__ int s_last;
   __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    s_last = atomicAdd(a.scan_done, 1u) == gridDim.x * gridDim.y - 1;
-  }
+  if (tid == 0) s_last = atom_add_acq_rel_gpu(a.scan_done, 1u) == gridDim.x * gridDim.y - 1;
   __syncthreads();
   if (s_last) {
-    __threadfence();
     const bool publish = (a.G > 1 || !a.counts_host) &&   // on one GPU k_hist already did
                          !(__ldcg(a.err) & kErrTimeout);   // never release incomplete counts
     if (publish && a.counts_host)
@@ -318,16 +316,14 @@ __global__ void __launch_bounds__(kThreads) k_scan(const __grid_constant__ ScanA
     __syncthreads();
     if (tid == 0) {
       *a.scan_done = 0;
-      if (publish) {
-        __threadfence_system();
-        st_release_sys(a.host_flag, a.epoch);
-      }
+      if (publish) st_release_sys(a.host_flag, a.epoch);  // after bar.sync: covers every thread's copies
     }
   }
 }
 
 struct ScatterArgs {
   int32_t *err;
+  int32_t nbits;  // bits of the largest expert id (ballot matching)
   const int32_t *ids;
   const float *gates;
   int64_t npairs;
@@ -345,15 +341,26 @@ __host__ __device__ constexpr size_t scatter_smem(int tile, int GS) {
   return (size_t)tile * (4 + 4 + 4 + 2) + (size_t)GS * 4 + 16;
 }
 
-__global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ ScatterArgs a) {
-  constexpr int kWarps = kThreads / 32;
+constexpr int kSThreads = 512;  // k_scatter block: 16 warps (shorter per-warp rank chains)
+
+// Per-expert constants of one tile, read with three 16-byte shared loads per pair.
+struct alignas(16) ExpTab {
+  int32_t Rb;    // global rank (within e) of the tile's first pair of e: base + tile prefix
+  int32_t toff;  // where e's pairs start in the tile's expert-sorted order
+  int32_t q, m;  // C_e / r_e, C_e % r_e
+  uint32_t rq1, rq;
+  int32_t fs;    // first slot of e (plan_t)
+  int32_t loc;   // where e's kept pairs start in this rank's send order
+  int32_t base;  // global rank of this rank's first pair of e
+  int32_t pad[3];
+};
+
+__global__ void __launch_bounds__(kSThreads) k_scatter(const __grid_constant__ ScatterArgs a) {
+  constexpr int kWarps = kSThreads / 32;
   __shared__ int16_t wcnt[kWarps][MOE_MAX_E];  // per-warp running counts (< tile <= 4096)
-  __shared__ ExpertInfo s_info[MOE_MAX_E];
-  __shared__ int32_t s_blk[MOE_MAX_E];
-  __shared__ int32_t s_loc[MOE_MAX_E];   // where expert e's kept pairs start in this rank's send order
-  __shared__ int32_t s_toff[MOE_MAX_E];  // where expert e's pairs start in this tile's expert-sorted order
-  __shared__ int32_t s_fs[MOE_MAX_E + 1];  // plan_t (lane-divergent reads: not from the param bank)
-  __shared__ int s_poisoned;
+  __shared__ ExpTab tab[MOE_MAX_E];
+  __shared__ int32_t s_tcnt[MOE_MAX_E];
+  __shared__ int s_poisoned, s_nsorted;
   extern __shared__ __align__(16) int32_t s_dyn[];
   int32_t *s_tile = s_dyn;                     // [tile] ids, then (rank << 8 | e) after pass 1
   int32_t *s_gate = s_dyn + a.tile;            // [tile] gate bit patterns
@@ -371,65 +378,74 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ Sc
     const int32_t *gp = reinterpret_cast<const int32_t *>(a.gates) + off_v + tbase;
     if ((((uintptr_t)ip | (uintptr_t)gp) & 15) == 0) {
       const int n4 = n >> 2;
-      for (int i = tid; i < n4; i += kThreads) {
+      for (int i = tid; i < n4; i += kSThreads) {
         reinterpret_cast<int4 *>(s_tile)[i] = __ldg(reinterpret_cast<const int4 *>(ip) + i);
         reinterpret_cast<int4 *>(s_gate)[i] = __ldg(reinterpret_cast<const int4 *>(gp) + i);
       }
-      for (int i = 4 * n4 + tid; i < n; i += kThreads) {
+      for (int i = 4 * n4 + tid; i < n; i += kSThreads) {
         s_tile[i] = __ldg(ip + i);
         s_gate[i] = __ldg(gp + i);
       }
     } else {
-      for (int i = tid; i < n; i += kThreads) {
+      for (int i = tid; i < n; i += kSThreads) {
         s_tile[i] = __ldg(ip + i);
         s_gate[i] = __ldg(gp + i);
       }
     }
   }
+  for (int i = tid; i < kWarps * MOE_MAX_E; i += kSThreads) (&wcnt[0][0])[i] = 0;
   pdl_wait();  // k_scan's outputs (einfo, scanned tile counts, kept_pre)
   if (tid == 0) s_poisoned = (__ldcg(a.err) & kErrTimeout) != 0;  // k_scan timed out: no outputs
-  for (int e = tid; e < a.E; e += kThreads) {
-    s_info[e] = a.einfo[v * a.E + e];
-    s_blk[e] = a.blk[((int64_t)v * a.E + e) * a.nb_max + b];
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) wcnt[w][e] = 0;
+  for (int e = tid; e < a.E; e += kSThreads) {
+    const ExpertInfo in = a.einfo[v * a.E + e];
+    ExpTab t;
+    t.Rb = in.base + a.blk[((int64_t)v * a.E + e) * a.nb_max + b];
+    t.q = in.q;
+    t.m = in.m;
+    t.rq1 = in.rq1;
+    t.rq = in.rq;
+    t.fs = a.fs[e];
+    t.base = in.base;
+    t.loc = in.kcnt;  // prefix-summed below
+    t.toff = 0;
+    tab[e] = t;
   }
-  for (int e = tid; e <= a.E; e += kThreads) s_fs[e] = a.fs[e];
-  for (int j = tid; j < a.GS; j += kThreads) s_kp[j] = a.kept_pre[(int64_t)v * a.GS + j];
+  for (int j = tid; j < a.GS; j += kSThreads) s_kp[j] = a.kept_pre[(int64_t)v * a.GS + j];
   __syncthreads();
   if (s_poisoned) return;
-  if (warp == 0) {  // s_loc = exclusive prefix over experts of this rank's kept counts
+  if (warp == 0) {  // loc = exclusive prefix over experts of this rank's kept counts
     constexpr int kPer = MOE_MAX_E / 32;
-    int32_t c[kPer], s = 0;
+    int32_t c[kPer], sum = 0;
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
       const int e = lane * kPer + i;
-      c[i] = e < a.E ? s_info[e].kcnt : 0;
-      s += c[i];
+      c[i] = e < a.E ? tab[e].loc : 0;
+      sum += c[i];
     }
-    int32_t incl = s;
+    int32_t incl = sum;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       const int32_t y = __shfl_up_sync(0xffffffffu, incl, d);
       if (lane >= d) incl += y;
     }
-    int32_t run = incl - s;
+    int32_t run = incl - sum;
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
       const int e = lane * kPer + i;
-      if (e < a.E) s_loc[e] = run;
+      if (e < a.E) tab[e].loc = run;
       run += c[i];
     }
   }
   const int32_t capv = a.cap > 0 ? a.cap : 0x7fffffff;
 
-  // Warp w owns the consecutive pairs [w*R*32, (w+1)*R*32) of the tile (R = tile/256 rounds of
-  // 32): pair order == (warp, round, lane) order, so the ranks below are stable.
-  // Pass 1 ranks each pair within its warp's pairs of the same expert -- the warp's running
-  // count of e before this round + the lower lanes of the round with e (__match_any_sync) --
-  // and packs (rank << 8 | e) into the staged id; an exclusive prefix over warps then turns
-  // the per-warp totals into starting ranks, and pass 2 needs no further matching.
-  const int rounds = a.tile / kThreads;
+  // Warp w owns the consecutive pairs [w*R*32, (w+1)*R*32) of the tile (R = tile/512 rounds
+  // of 32): pair order == (warp, round, lane) order, so the ranks below are stable.
+  // Pass 1 ranks each pair within its warp's pairs of the same expert: the warp's running
+  // count of e before this round + the lower lanes of the round holding e.  The lanes holding
+  // e come from ceil(log2 E) ballots (one per bit of the expert id: no long-latency match);
+  // the rank is packed as (rank << 8 | e) into the staged id, an exclusive prefix over warps
+  // then turns the per-warp totals into starting ranks, and pass 2 needs no further matching.
+  const int rounds = a.tile / kSThreads;
   const int seg = warp * rounds * 32;
   const unsigned lt = (1u << lane) - 1u;
   for (int r = 0; r < rounds; ++r) {  // pass 1
@@ -437,23 +453,29 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ Sc
     const bool in = p < n;
     const int e = in ? s_tile[p] : -1;
     const bool valid = in && (unsigned)e < (unsigned)a.E;
-    const unsigned act = __ballot_sync(0xffffffffu, valid);
-    unsigned peers = 0;
-    int32_t wr = 0;
+    unsigned peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+    for (int bit = 0; bit < 8; ++bit) {
+      if (bit < a.nbits) {  // warp-uniform
+        const bool on = (e >> bit) & 1;
+        const unsigned bal = __ballot_sync(0xffffffffu, on);
+        peers &= on ? bal : ~bal;
+      }
+    }
     if (valid) {
-      peers = __match_any_sync(act, e);
-      wr = wcnt[warp][e] + __popc(peers & lt);
+      const int32_t wr = wcnt[warp][e] + __popc(peers & lt);
+      s_tile[p] = (wr << 8) | e;  // E <= 256, wr < tile
+    } else if (in) {
+      s_tile[p] = -1;
     }
     __syncwarp();
-    if (valid && lane == __ffs(peers) - 1) wcnt[warp][e] = (int16_t)(wcnt[warp][e] + __popc(peers));
-    if (in) s_tile[p] = valid ? (wr << 8) | e : -1;  // E <= 256, wr < tile
+    if (valid && (peers & lt) == 0) wcnt[warp][e] = (int16_t)(wcnt[warp][e] + __popc(peers));
     __syncwarp();
   }
   __syncthreads();
   // exclusive prefix over warps, per expert (-> starting rank of each warp's pairs of e inside
   // the tile), and the tile's count of e
-  __shared__ int32_t s_tcnt[MOE_MAX_E];
-  for (int e = tid; e < a.E; e += kThreads) {
+  for (int e = tid; e < a.E; e += kSThreads) {
     int32_t run = 0;
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) {
@@ -464,28 +486,29 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ Sc
     s_tcnt[e] = run;
   }
   __syncthreads();
-  if (warp == 0) {  // s_toff = exclusive prefix over experts of the tile counts
+  if (warp == 0) {  // toff = exclusive prefix over experts of the tile counts
     constexpr int kPer = MOE_MAX_E / 32;
-    int32_t c[kPer], s = 0;
+    int32_t c[kPer], sum = 0;
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
       const int e = lane * kPer + i;
       c[i] = e < a.E ? s_tcnt[e] : 0;
-      s += c[i];
+      sum += c[i];
     }
-    int32_t incl = s;
+    int32_t incl = sum;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       const int32_t y = __shfl_up_sync(0xffffffffu, incl, d);
       if (lane >= d) incl += y;
     }
-    int32_t run = incl - s;
+    int32_t run = incl - sum;
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
       const int e = lane * kPer + i;
-      if (e < a.E) s_toff[e] = run;
+      if (e < a.E) tab[e].toff = run;
       run += c[i];
     }
+    if (lane == 31) s_nsorted = run;  // valid pairs of the tile
   }
   __syncthreads();
   // Pass 2: per pair (slot, offset) -- written in pair order (coalesced) -- and its send
@@ -502,16 +525,15 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ Sc
     }
     const int e = x & 0xff;
     const int32_t tr = wcnt[warp][e] + (x >> 8);  // rank of the pair among the tile's pairs of e
-    const ExpertInfo info = s_info[e];
-    const int32_t lr = s_blk[e] + tr;  // rank within this rank's pairs of e
-    const int32_t R = info.base + lr;  // global rank within expert e
-    const int32_t q = info.q, m = info.m;
+    const ExpTab t = tab[e];
+    const int32_t R = t.Rb + tr;  // global rank within expert e
+    const int32_t q = t.q, m = t.m;
     const int32_t big = m * (q + 1);
-    const int32_t rho = R < big ? (int32_t)udiv_fast((uint32_t)R, (uint32_t)(q + 1), info.rq1)
-                                : m + (int32_t)udiv_fast((uint32_t)(R - big), (uint32_t)q, info.rq);
+    const int32_t rho = R < big ? (int32_t)udiv_fast((uint32_t)R, (uint32_t)(q + 1), t.rq1)
+                                : m + (int32_t)udiv_fast((uint32_t)(R - big), (uint32_t)q, t.rq);
     const int32_t start = rho * q + min(rho, m);
     const int32_t off = R - start;
-    const int32_t si = s_toff[e] + tr;
+    const int32_t si = t.toff + tr;
     st_pair[si] = (uint16_t)p;
     if (off >= capv) {  // row f2: beyond the replica's capacity -> dropped, not sent
       dslot[p] = -1;
@@ -519,19 +541,19 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ Sc
       st_pos[si] = -1;
       continue;
     }
-    const int32_t slot = s_fs[e] + rho;
+    const int32_t slot = t.fs + rho;
     dslot[p] = slot;
     doff[p] = off;
     // slot-major position among this rank's kept pairs: experts before e, kept pairs of this
     // rank in e's earlier replicas, then this rank's pairs in replica rho before this one
     // (all kept: a replica keeps a prefix of its offsets)
-    st_pos[si] = s_loc[e] + s_kp[slot] + (R - max(info.base, start));
+    st_pos[si] = t.loc + s_kp[slot] + (R - max(t.base, start));
   }
   __syncthreads();
   // Pass 3: send_pair / send_gate in the expert-sorted order.  Consecutive sorted entries of one
   // expert go to consecutive send positions, so the stores form contiguous runs.
-  const int nsorted = s_toff[a.E - 1] + s_tcnt[a.E - 1];  // valid pairs of the tile
-  for (int i = tid; i < nsorted; i += kThreads) {
+  const int nsorted = s_nsorted;
+  for (int i = tid; i < nsorted; i += kSThreads) {
     const int32_t pos = st_pos[i];
     if (pos < 0) continue;
     const int p = st_pair[i];
@@ -560,10 +582,10 @@ namespace {
 // tail of the previous kernel in the stream; the kernel calls pdl_wait() before reading it.
 template <typename Args>
 cudaError_t launch_pdl(void (*kern)(Args), dim3 grid, cudaStream_t s, const Args &args,
-                       size_t smem = 0) {
+                       size_t smem = 0, int threads = kThreads) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -598,7 +620,7 @@ extern "C" int moe_dispatch(moe_ctx *ctx, const int32_t *topk_ids, const float *
   // little atomic traffic), small inputs still fill the GPU.
   const int64_t per_rank_tiles = std::max<int64_t>(1, (int64_t)4 * ctx->num_sms / ctx->n_local);
   int64_t tile = (npairs + per_rank_tiles - 1) / per_rank_tiles;
-  tile = std::max<int64_t>(kTilePairs, (tile + kThreads - 1) / kThreads * kThreads);
+  tile = std::max<int64_t>(kTilePairs, (tile + kTilePairs - 1) / kTilePairs * kTilePairs);  // k_scatter: 512 threads
   tile = std::min<int64_t>(tile, kMaxTilePairs);  // k_scatter stages ids + gates in smem
   const int nb = (int)std::max<int64_t>(1, (npairs + tile - 1) / tile);
   const int real = ctx->rank >= 0 ? 1 : 0;
@@ -669,6 +691,8 @@ extern "C" int moe_dispatch(moe_ctx *ctx, const int32_t *topk_ids, const float *
 
   ScatterArgs ca{};
   ca.err = ctx->err;
+  ca.nbits = 1;
+  while ((1 << ca.nbits) < ctx->E) ++ca.nbits;
   ca.ids = topk_ids;
   ca.gates = gates;
   ca.npairs = npairs;
@@ -687,7 +711,8 @@ extern "C" int moe_dispatch(moe_ctx *ctx, const int32_t *topk_ids, const float *
   ca.kept_pre = ctx->kept_pre;
   for (int e = 0; e <= ctx->E; ++e) ca.fs[e] = plan->first_slot[e];
   if (npairs > 0)
-    MOE_CUDA_TRY(launch_pdl(k_scatter, dim3(nb, ctx->n_local), s, ca, scatter_smem((int)tile, ctx->G * ctx->S)));
+    MOE_CUDA_TRY(launch_pdl(k_scatter, dim3(nb, ctx->n_local), s, ca, scatter_smem((int)tile, ctx->G * ctx->S),
+                            kSThreads));
   timing_end(ctx->ev_disp, tev, s);
   return MOE_OK;
 }

@@ -65,6 +65,7 @@ struct moe_ctx {
   int update_kernel;  // 1: k_update_tma (bulk-copy rings, default); 0: k_update (register-staged)
   bool connected;
   uint32_t disp_epoch, upd_epoch;
+  int32_t sched_policy, sched_interval;  // moe_ctx_set_schedule (row f2)
 
   // caller buffers, per local rank
   std::vector<void *> slot_w, slot_g;

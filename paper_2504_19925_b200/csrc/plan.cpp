@@ -148,6 +148,45 @@ extern "C" int moe_plan_ex(const int64_t *counts, int32_t E, int32_t G, int32_t 
   return MOE_OK;
 }
 
+extern "C" int moe_plan_scheduled(const int64_t *counts, const moe_plan_t *plan_cur, int32_t policy,
+                                  int32_t replan_interval, int64_t step, moe_plan_t *plan_next,
+                                  int32_t *replanned) {
+  if (!counts || !plan_cur || !plan_next || !plan_cur->replicas || !plan_cur->first_slot ||
+      !plan_cur->slot_expert || !plan_next->replicas || !plan_next->first_slot || !plan_next->slot_expert)
+    return moe::fail(MOE_ERR_INVALID, "moe_plan_scheduled: NULL pointer");
+  if (step < 1 || replan_interval < 1)
+    return moe::fail(MOE_ERR_INVALID, "moe_plan_scheduled: step and replan_interval must be >= 1");
+  if (policy != MOE_PLAN_PAPER_ALG1 && policy != MOE_PLAN_MINMAX && policy != MOE_PLAN_STATIC)
+    return moe::fail(MOE_ERR_INVALID, "moe_plan_scheduled: policy %d is not a placement policy", policy);
+  const int32_t E = plan_cur->E, G = plan_cur->G, S = plan_cur->S;
+  if (E < 1 || G < 1 || S < 1 || E > MOE_MAX_E || (int64_t)G * S > MOE_MAX_SLOTS || E > G * S)
+    return moe::fail(MOE_ERR_SHAPE, "moe_plan_scheduled: plan_cur E/G/S invalid");
+  const int32_t GS = G * S;
+  // plan_cur must be a contiguous placement: first_slot prefix of replicas >= 1, slot map
+  if (plan_cur->first_slot[0] != 0 || plan_cur->first_slot[E] != GS)
+    return moe::fail(MOE_ERR_SHAPE, "moe_plan_scheduled: plan_cur first_slot invalid");
+  for (int e = 0; e < E; ++e) {
+    const int32_t a = plan_cur->first_slot[e], b = plan_cur->first_slot[e + 1];
+    if (b - a < 1 || plan_cur->replicas[e] != b - a)
+      return moe::fail(MOE_ERR_SHAPE, "moe_plan_scheduled: plan_cur expert %d invalid", e);
+    for (int32_t j = a; j < b; ++j)
+      if (plan_cur->slot_expert[j] != e) return moe::fail(MOE_ERR_SHAPE, "moe_plan_scheduled: slot map");
+  }
+  const bool replan = step % replan_interval == 0;
+  if (replanned) *replanned = replan ? 1 : 0;
+  if (replan) return moe_plan_ex(counts, E, G, S, policy, plan_next, nullptr);
+  // keep: plan_{t+1} = plan_t (the update still runs, placing into the same slots)
+  if (plan_next != plan_cur) {
+    std::memmove(plan_next->replicas, plan_cur->replicas, sizeof(int32_t) * E);
+    std::memmove(plan_next->first_slot, plan_cur->first_slot, sizeof(int32_t) * (E + 1));
+    std::memmove(plan_next->slot_expert, plan_cur->slot_expert, sizeof(int32_t) * GS);
+    plan_next->E = E;
+    plan_next->G = G;
+    plan_next->S = S;
+  }
+  return MOE_OK;
+}
+
 extern "C" int32_t moe_slot_capacity(double cf, int64_t T, int32_t k, int32_t G, int32_t S) {
   if (!(cf > 0.0) || T < 0 || k < 1 || G < 1 || S < 1) return -1;
   const double c = std::floor(cf * (double)T * (double)k / ((double)G * (double)S));
@@ -176,3 +215,10 @@ extern "C" const char *moe_status_str(int status) {
 extern "C" const char *moe_last_error(void) { return moe::last_error_buf().c_str(); }
 
 extern "C" int moe_abi_version(void) { return MOE_ABI_VERSION; }
+
+#ifndef MOE_BUILD_ID
+#define MOE_BUILD_ID "unknown-build-id"
+#endif
+// "MOEDC_BUILD_ID=<16 hex>" is also searched for in the file by _build.built_id()
+static const char kBuildTag[] = "MOEDC_BUILD_ID=" MOE_BUILD_ID;
+extern "C" const char *moe_build_id(void) { return kBuildTag + 15; }

@@ -29,22 +29,17 @@ extern "C" int moe_step(moe_ctx *ctx, const int32_t *topk_ids, const float *gate
   st = moe_ctx_wait_counts(ctx);  // C_t on the host
   if (st) return moe_step_abort(ctx, st);
   const auto t1 = clk::now();
-  if (policy == MOE_PLAN_KEEP) {  // interval policy between re-plans: plan_{t+1} = plan_t
-    if (!plan_next->replicas || !plan_next->first_slot || !plan_next->slot_expert || !plan_cur->replicas ||
-        !plan_cur->slot_expert)
-      return moe::fail(MOE_ERR_INVALID, "moe_step: NULL plan array");
-    const int32_t E = plan_cur->E, GS = plan_cur->G * plan_cur->S;
-    for (int e = 0; e < E; ++e) plan_next->replicas[e] = plan_cur->replicas[e];
-    for (int e = 0; e <= E; ++e) plan_next->first_slot[e] = plan_cur->first_slot[e];
-    for (int j = 0; j < GS; ++j) plan_next->slot_expert[j] = plan_cur->slot_expert[j];
-    plan_next->E = E;
-    plan_next->G = plan_cur->G;
-    plan_next->S = plan_cur->S;
+  if (policy == MOE_PLAN_SCHEDULED) {  // the library's schedule decides (row f2, reading B3)
+    int32_t sp = 0, si = 1;
+    moe_ctx_schedule(ctx, &sp, &si);
+    st = moe_plan_scheduled(out->counts_host, plan_cur, sp, si, adam->step, plan_next, nullptr);
+  } else if (policy == MOE_PLAN_KEEP) {  // plan_{t+1} = plan_t
+    st = moe_plan_scheduled(out->counts_host, plan_cur, MOE_PLAN_PAPER_ALG1, 1 << 30, 1, plan_next, nullptr);
   } else {
     st = moe_plan_ex(out->counts_host, plan_cur->E, plan_cur->G, plan_cur->S, policy, plan_next,
                      nullptr);  // a1 -> plan_{t+1}
-    if (st) return moe_step_abort(ctx, st);
   }
+  if (st) return moe_step_abort(ctx, st);
   const auto t2 = clk::now();
   st = moe_update(ctx, plan_cur, plan_next, adam, stream);  // a3 + a4 + a5
   moe_host_time(ctx, 0, std::chrono::duration<double, std::milli>(t1 - t0).count());

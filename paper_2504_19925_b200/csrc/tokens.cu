@@ -242,30 +242,55 @@ __device__ __forceinline__ void tok_accum(const TokArgs &a, float (&acc)[U][8], 
 // them into a row pointer (nullptr when dropped); the warp then walks the row in chunks of
 // 32 x kCombU vectors, loading two rows' chunks before accumulating either (shuffled
 // pointers), fp32 adds in ascending j (reading C2).  k > 32 falls back to per-pair loads.
+// Lane j < k's row pointer and gate for pair j of global token index tk (nullptr: dropped).
+__device__ __forceinline__ void comb_src(const TokArgs &a, uint32_t tk, int lane, const uint4 *&row, float &g) {
+  row = nullptr;
+  g = 1.f;
+  if (lane >= a.k || lane >= 32) return;
+  const uint32_t v = tk / (uint32_t)a.T;
+  const int64_t p = ((int64_t)v * a.T + (tk - v * (uint32_t)a.T)) * a.k + lane;
+  const int s = __ldg(a.dest_slot + p);
+  if (s < 0) return;  // dropped pairs contribute nothing
+  const int off = __ldg(a.dest_off + p);
+  if (off >= a.rows) {
+    atomicOr(a.err, kErrData);
+    return;
+  }
+  const uint32_t h = (uint32_t)s / (uint32_t)a.S;
+  row = a.xb[h] + ((int64_t)((uint32_t)s - h * (uint32_t)a.S) * a.rows + off) * a.dv;
+  if (a.gate) g = __ldg(a.gates + p);
+}
+
+// Bulk-copy engine prefetch of a whole row (local or peer HBM) into this GPU's L2.
+__device__ __forceinline__ void prefetch_row_l2(const uint4 *row, int64_t dv) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(row), "r"((uint32_t)(dv * 16)) : "memory");
+}
+
+// A warp per token (grid stride).  Lanes j < k fetch pair j's slot/offset/gate once and turn
+// them into a row pointer (nullptr when dropped); the warp then walks the row in chunks of
+// 32 x kCombU vectors, loading two rows' chunks before accumulating either (shuffled
+// pointers), fp32 adds in ascending j (reading C2).  k > 32 falls back to per-pair loads.
+// While token t is summed, the bulk-copy engine already prefetches the k rows of the warp's
+// next token into L2 (one cp.async.bulk.prefetch per row), so its loads are L2 hits.
 template <int U>
 __global__ void __launch_bounds__(kThreads, 4) k_tok_combine(TokArgs a) {
   arrive_and_wait(a);
   const int lane = threadIdx.x & 31;
   const uint32_t warps = gridDim.x * (kThreads / 32);
   const uint32_t ntok = (uint32_t)(a.T * a.n_local);  // < 2^31 (moe_ctx_create)
-  for (uint32_t tok = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); tok < ntok; tok += warps) {
+  uint32_t tok = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  const uint4 *nx_row = nullptr;
+  float nx_g = 1.f;
+  if (tok < ntok) comb_src(a, tok, lane, nx_row, nx_g);
+  for (; tok < ntok; tok += warps) {
     const uint32_t v = tok / (uint32_t)a.T;
     const uint32_t t = tok - v * (uint32_t)a.T;
     const int64_t pbase = ((int64_t)v * a.T + t) * a.k;
-    const uint4 *my_row = nullptr;
-    float my_g = 1.f;
-    if (lane < a.k && lane < 32) {
-      const int s = __ldg(a.dest_slot + pbase + lane);
-      if (s >= 0) {  // dropped pairs contribute nothing
-        const int off = __ldg(a.dest_off + pbase + lane);
-        if (off < a.rows) {
-          const uint32_t h = (uint32_t)s / (uint32_t)a.S;
-          my_row = a.xb[h] + ((int64_t)((uint32_t)s - h * (uint32_t)a.S) * a.rows + off) * a.dv;
-          if (a.gate) my_g = __ldg(a.gates + pbase + lane);
-        } else {
-          atomicOr(a.err, kErrData);
-        }
-      }
+    const uint4 *my_row = nx_row;
+    const float my_g = nx_g;
+    if (tok + warps < ntok) {
+      comb_src(a, tok + warps, lane, nx_row, nx_g);
+      if (nx_row) prefetch_row_l2(nx_row, a.dv);
     }
     uint4 *dst = a.dst[v] + (int64_t)t * a.dv;
     for (int64_t c0 = 0; c0 < a.dv; c0 += 32 * U) {

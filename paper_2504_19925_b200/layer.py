@@ -69,6 +69,7 @@ class DecoupledExpertLayer:
                                   self.master, self.adam_m, self.adam_v, device=device,
                                   options=opts)
         self.dedup = dedup
+        self.ctx.set_schedule(policy, replan_interval)  # the library decides re-place vs keep
         self.out = api.DispatchBuffers(self.ctx, max_tokens, capacity=capacity)
         self.seed = seed
         if init_master:
@@ -95,15 +96,11 @@ class DecoupledExpertLayer:
         api.moe_dispatch(self.ctx, topk_ids, gates, T, self.plan, self.out, stream)
         return self.out
 
-    def _replans(self) -> bool:
-        """Interval policy (reading B3): re-place after iterations t = i, 2i, ..."""
-        return self.t % self.replan_interval == 0
-
     def plan_next(self) -> api.Plan:
+        """a1 for the split-call path: wait for C_t, then the library's schedule (row f2)."""
         self.ctx.wait_counts()
-        if not self._replans():
-            return api.Plan.from_first_slot(self.plan.first_slot, self.G, self.S)
-        return api.moe_plan(self.out.counts_host.numpy(), self.E, self.G, self.S, self.policy)
+        return api.moe_plan_scheduled(self.out.counts_host.numpy(), self.plan, self.policy,
+                                      self.replan_interval, self.t)
 
     def update(self, plan_next: api.Plan, stream=None) -> None:
         api.moe_update(self.ctx, self.plan, plan_next, self.adam, self.t, self.scale_mode,
@@ -116,8 +113,7 @@ class DecoupledExpertLayer:
         dispatch -> host plan (overlapping the scatter kernel) -> reduce/Adam/place."""
         if not self._connected:
             raise RuntimeError("real-mode layer: call connect() first")
-        policy = self.policy if self._replans() else api.MOE_PLAN_KEEP
-        nxt = api.moe_step(self.ctx, topk_ids, gates, T, self.plan, policy, self.out, self.adam,
+        nxt = api.moe_step(self.ctx, topk_ids, gates, T, self.plan, api.MOE_PLAN_SCHEDULED, self.out, self.adam,
                            self.t, self.scale_mode, self.scale, stream)
         self.plan = nxt
         self.t += 1

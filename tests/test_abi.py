@@ -37,7 +37,9 @@ def test_exports_every_declared_symbol(lib):
     assert declared == set(_lib.EXPORTED)
     for name in declared:
         assert hasattr(lib, name), name
-    assert lib.moe_abi_version() == 5
+    assert lib.moe_abi_version() == 6
+    from paper_2504_19925_b200 import _build
+    assert lib.moe_build_id().decode() == _build.source_hash() == _build.built_id()
     assert lib.moe_status_str(3) == b"MOE_ERR_DATA"
     assert lib.moe_ctx_handle_bytes() >= 3 * 64
 
@@ -124,3 +126,43 @@ def test_spec_examples_through_abi(lib, golden_dir):
     for ex in g["compute_placement"]:
         p = api.moe_plan(np.array(ex["popularity"]), len(ex["popularity"]), 1, ex["slots_total"])
         assert p.replicas.tolist() == ex["replicas"], ex["cite"]
+
+
+def test_interval_schedule_is_decided_by_the_library(lib):
+    """Row f2, reading B3: moe_plan_scheduled re-places with the policy after iterations t with
+    t % i == 0 and keeps plan_t otherwise -- the oracle's interval policy (OracleSim: re-plan
+    iff step % replan_interval == 0), over random count sequences, every policy."""
+    from paper_2504_19925_b200 import api
+    rng = np.random.default_rng(7)
+    names = {0: "alg1", 1: "minmax", 2: "static"}
+    for case in range(60):
+        E = int(rng.integers(1, 20))
+        G = int(rng.integers(1, 5))
+        S = -(-E // G) + int(rng.integers(0, 4))
+        pol = int(rng.integers(0, 3))
+        interval = int(rng.choice([1, 2, 3, 5]))
+        cur = api.moe_plan(np.zeros(E, np.int64), E, G, S, pol)
+        want = OP.plan(np.ones(E, np.int64), E, G, S, names[pol])
+        for t in range(1, 13):
+            C_t = rng.integers(0, 1000, E).astype(np.int64)
+            nxt = api.moe_plan_scheduled(C_t, cur, pol, interval, t)
+            want = OP.plan(C_t, E, G, S, names[pol]) if t % interval == 0 else want
+            assert nxt.replicas.tolist() == want["replicas"].tolist(), (case, t)
+            assert nxt.first_slot.tolist() == want["first_slot"].tolist()
+            assert nxt.slot_expert.tolist() == want["slot_expert"].tolist()
+            cur = nxt
+
+
+def test_interval_schedule_errors(lib):
+    from paper_2504_19925_b200 import api
+    from paper_2504_19925_b200._lib import MoeError
+    cur = api.moe_plan(np.ones(4, np.int64), 4, 2, 2)
+    c = np.ones(4, np.int64)
+    for bad in ((0, 0, 1), (3, 1, 1), (4, 1, 1), (0, 1, 0)):   # (policy, interval, step)
+        with pytest.raises(MoeError) as ei:
+            api.moe_plan_scheduled(c, cur, bad[0], bad[1], bad[2])
+        assert ei.value.status == 1
+    cur.first_slot[2] = cur.first_slot[1]          # an expert without a replica
+    with pytest.raises(MoeError) as ei:
+        api.moe_plan_scheduled(c, cur, 0, 2, 1)
+    assert ei.value.status == 2

@@ -27,6 +27,8 @@ def test_cuda_extension_is_the_path():
     assert os.path.samefile(L._name, _lib.LIB_PATH)
     maps = open("/proc/self/maps").read()
     assert "libmoedc.so" in maps
+    from paper_2504_19925_b200 import _build   # the loaded binary was built from HEAD's sources
+    assert L.moe_build_id().decode() == _build.source_hash()
 
 
 @pytest.mark.parametrize("name", ["tiny", "tiny-skew", "tiny-odd"])

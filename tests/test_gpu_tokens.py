@@ -11,6 +11,17 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.fixture(scope="module", autouse=True)
+
+def _plan_from_oracle(p, G, S):
+    """The oracle's placement (replicas, first_slot, slot_expert) as a moe_plan_t for the layer."""
+    from paper_2504_19925_b200 import api
+    E = len(p["replicas"])
+    pl = api.Plan(E, G, S)
+    pl.replicas[:] = p["replicas"]
+    pl.first_slot[:] = p["first_slot"]
+    pl.slot_expert[:] = p["slot_expert"]
+    return pl
+
 def _built():
     import __graft_entry__
     __graft_entry__.build()
@@ -58,7 +69,7 @@ def run_tokens(name, G: int, iters: int, cf: float = 0.0, flags: int = 0, T: int
     rng = np.random.default_rng(seed + 17)
     use_gate = bool(flags & api.MOE_TOK_GATE)
     for it, ((ids, gates), (plan_t, disp)) in enumerate(zip(tr, routes)):
-        layer.plan = api.Plan.from_first_slot(plan_t["first_slot"], G, S)
+        layer.plan = _plan_from_oracle(plan_t, G, S)
         ids_d = torch.from_numpy(np.ascontiguousarray(ids)).cuda()
         gates_d = torch.from_numpy(np.ascontiguousarray(gates)).cuda()
         layer.dispatch(ids_d, gates_d, Tg)
@@ -141,7 +152,7 @@ def test_special_values_bitwise():
     disp = OD.dispatch([ids], [gates], plan["first_slot"], E)
     rows = int(disp["slot_load"].max())
     layer = DecoupledExpertLayer(E, G, S, k, 8, T, rank=0, device=0)
-    layer.plan = api.Plan.from_first_slot(plan["first_slot"], G, S)
+    layer.plan = _plan_from_oracle(plan, G, S)
     gates_d = torch.from_numpy(gates).cuda()
     layer.dispatch(torch.from_numpy(ids).cuda(), gates_d, T)
     tx = TokenExchange(layer.ctx, d, rows)
