@@ -371,9 +371,14 @@ def token_a2a(args, wl, layer, gates, G, rank, Tg, S, peak_hbm, barrier, stream)
         dist.all_reduce(rows_t, op=dist.ReduceOp.MAX)
     rows = max(1, int(rows_t.item()))
     need = S * rows * d * 2
-    if need > (48 << 30):  # drop-free routing can pile a hot expert onto one replica
+    free = torch.cuda.mem_get_info()[0]
+    fits = torch.tensor([1 if need < 0.85 * free else 0], device="cuda")
+    if G > 1:
+        dist.all_reduce(fits, op=dist.ReduceOp.MIN)
+    if not int(fits.item()):  # drop-free routing can pile a hot expert onto one replica
         return {"skipped": f"the last iteration's hottest slot has {rows} rows: expert buffers "
-                           f"would need {need / 2**30:.0f} GiB per GPU (use --cf for a capacity)"}
+                           f"would need {need / 2**30:.0f} GiB per GPU, more than is free "
+                           f"(use --cf for a capacity)"}
     tx = TokenExchange(layer.ctx, d, rows)
     tx.connect_process_group()
     g = torch.Generator(device="cuda").manual_seed(1234 + rank)

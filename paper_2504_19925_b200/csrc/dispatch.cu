@@ -36,6 +36,7 @@ __device__ __forceinline__ uint32_t atom_add_acq_rel_gpu(uint32_t *p, uint32_t v
 }
 
 struct HistArgs {
+  int32_t sum_last;  // E * nb small: the last block sums the tile counts instead of atomics
   const int32_t *ids;
   int64_t npairs;  // pairs per rank = T*k
   int32_t k, E, G, rank, real, nb, nb_max, tile;
@@ -118,7 +119,7 @@ __global__ void __launch_bounds__(kThreads) k_hist(const __grid_constant__ HistA
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) h += whist[w][e];
     blk[(int64_t)e * a.nb_max + b] = h;
-    if (h) atomicAdd(a.cnt_local + v * a.E + e, h);
+    if (h && !a.sum_last) atomicAdd(a.cnt_local + v * a.E + e, h);
   }
   // ticket: bar.sync orders the block's writes before thread 0's acq_rel atomic (release is
   // cumulative); the last block's acquire makes every block's counts visible to it
@@ -129,8 +130,21 @@ __global__ void __launch_bounds__(kThreads) k_hist(const __grid_constant__ HistA
 
   // Last tile of rank v: publish the rank's counts (a0).
   const int grank = a.real ? a.rank : v;
+  if (a.sum_last) {  // few tiles x experts: the last block sums the tile counts (no atomics)
+    const int lane = tid & 31;
+    for (int e = warp; e < a.E; e += kWarps) {
+      const int32_t *row = blk + (int64_t)e * a.nb_max;
+      int32_t c = 0;
+      for (int i = lane; i < a.nb; i += 32) c += __ldcg(row + i);
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) c += __shfl_xor_sync(0xffffffffu, c, d);
+      if (lane == 0) whist[0][e] = c;
+    }
+    __syncthreads();
+  }
   for (int e = tid; e < a.E; e += kThreads) {
-    const int32_t c = atomicExch(a.cnt_local + v * a.E + e, 0);  // read + reset for next call
+    const int32_t c = a.sum_last ? whist[0][e]
+                                 : atomicExch(a.cnt_local + v * a.E + e, 0);  // read + reset for next call
     if (a.real) {
       for (int h = 0; h < a.G; ++h) a.dst[h]->xcnt[a.parity][grank][e] = c;  // NVLink stores
     } else {
@@ -323,7 +337,6 @@ __global__ void __launch_bounds__(kThreads) k_scan(const __grid_constant__ ScanA
 
 struct ScatterArgs {
   int32_t *err;
-  int32_t nbits;  // bits of the largest expert id (ballot matching)
   const int32_t *ids;
   const float *gates;
   int64_t npairs;
@@ -438,39 +451,48 @@ __global__ void __launch_bounds__(kSThreads) k_scatter(const __grid_constant__ S
   }
   const int32_t capv = a.cap > 0 ? a.cap : 0x7fffffff;
 
-  // Warp w owns the consecutive pairs [w*R*32, (w+1)*R*32) of the tile (R = tile/512 rounds
-  // of 32): pair order == (warp, round, lane) order, so the ranks below are stable.
+  // Warp w owns the consecutive pairs [w*R*32, (w+1)*R*32) of the tile (R = tile/512 <= 8
+  // rounds of 32): pair order == (warp, round, lane) order, so the ranks below are stable.
   // Pass 1 ranks each pair within its warp's pairs of the same expert: the warp's running
   // count of e before this round + the lower lanes of the round holding e.  The lanes holding
-  // e come from ceil(log2 E) ballots (one per bit of the expert id: no long-latency match);
-  // the rank is packed as (rank << 8 | e) into the staged id, an exclusive prefix over warps
-  // then turns the per-warp totals into starting ranks, and pass 2 needs no further matching.
+  // e (__match_any_sync) are found for all R rounds first -- independent, so their latencies
+  // overlap -- and only then chained through the per-warp counters.  The rank is packed as
+  // (rank << 8 | e) into the staged id; an exclusive prefix over warps then turns the per-warp
+  // totals into starting ranks, and pass 2 needs no further matching.
   const int rounds = a.tile / kSThreads;
   const int seg = warp * rounds * 32;
   const unsigned lt = (1u << lane) - 1u;
-  for (int r = 0; r < rounds; ++r) {  // pass 1
-    const int p = seg + r * 32 + lane;
-    const bool in = p < n;
-    const int e = in ? s_tile[p] : -1;
-    const bool valid = in && (unsigned)e < (unsigned)a.E;
-    unsigned peers = __ballot_sync(0xffffffffu, valid);
+  {  // pass 1
+    constexpr int kMaxRounds = kMaxTilePairs / kSThreads;
+    int er[kMaxRounds];
+    unsigned pr[kMaxRounds];
 #pragma unroll
-    for (int bit = 0; bit < 8; ++bit) {
-      if (bit < a.nbits) {  // warp-uniform
-        const bool on = (e >> bit) & 1;
-        const unsigned bal = __ballot_sync(0xffffffffu, on);
-        peers &= on ? bal : ~bal;
+    for (int r = 0; r < kMaxRounds; ++r) {
+      er[r] = -1;
+      pr[r] = 0;
+      if (r < rounds) {  // warp-uniform
+        const int p = seg + r * 32 + lane;
+        const int e = p < n ? s_tile[p] : -1;
+        const bool valid = (unsigned)e < (unsigned)a.E;
+        const unsigned act = __ballot_sync(0xffffffffu, valid);
+        if (valid) {
+          pr[r] = __match_any_sync(act, e);
+          er[r] = e;
+        }
       }
     }
-    if (valid) {
-      const int32_t wr = wcnt[warp][e] + __popc(peers & lt);
-      s_tile[p] = (wr << 8) | e;  // E <= 256, wr < tile
-    } else if (in) {
-      s_tile[p] = -1;
+#pragma unroll
+    for (int r = 0; r < kMaxRounds; ++r) {
+      if (r < rounds) {
+        const int p = seg + r * 32 + lane;
+        const int e = er[r];
+        if (e >= 0) s_tile[p] = ((wcnt[warp][e] + __popc(pr[r] & lt)) << 8) | e;  // E <= 256, rank < tile
+        else if (p < n) s_tile[p] = -1;
+        __syncwarp();
+        if (e >= 0 && (pr[r] & lt) == 0) wcnt[warp][e] = (int16_t)(wcnt[warp][e] + __popc(pr[r]));
+        __syncwarp();
+      }
     }
-    __syncwarp();
-    if (valid && (peers & lt) == 0) wcnt[warp][e] = (int16_t)(wcnt[warp][e] + __popc(peers));
-    __syncwarp();
   }
   __syncthreads();
   // exclusive prefix over warps, per expert (-> starting rank of each warp's pairs of e inside
@@ -639,6 +661,7 @@ extern "C" int moe_dispatch(moe_ctx *ctx, const int32_t *topk_ids, const float *
   const int parity = (int)(epoch & 1u);
 
   HistArgs ha{};
+  ha.sum_last = (int64_t)ctx->E * nb <= 16384 ? 1 : 0;
   ha.ids = topk_ids;
   ha.npairs = npairs;
   ha.k = ctx->k;
@@ -691,8 +714,6 @@ extern "C" int moe_dispatch(moe_ctx *ctx, const int32_t *topk_ids, const float *
 
   ScatterArgs ca{};
   ca.err = ctx->err;
-  ca.nbits = 1;
-  while ((1 << ca.nbits) < ctx->E) ++ca.nbits;
   ca.ids = topk_ids;
   ca.gates = gates;
   ca.npairs = npairs;

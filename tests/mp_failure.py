@@ -35,6 +35,8 @@ def main() -> int:
     synth_grads(layer.slot_g[0], 1, 0, rank * S, S, P)
     layer.iterate(ids, gates, Tg)              # iteration 0: everyone
     layer.ctx.check()
+    snap = {n: getattr(layer.out, n).clone() for n in ("dest_slot", "dest_off", "send_pair", "send_gate",
+                                                       "send_count", "slot_load")}
     dist.barrier()
     ok = True
     if rank == 0:                              # iteration 1: rank 1 does not show up
@@ -50,6 +52,13 @@ def main() -> int:
         torch.cuda.synchronize()               # the GPU is not hung
         x = torch.ones(1 << 20, device="cuda").sum().item()
         ok = ok and x == float(1 << 20)
+        # memory intact: after the count-exchange timeout the scan and scatter wrote nothing
+        # (moe_dc.h: outputs keep their previous contents, nothing outside them is touched)
+        for n, v in snap.items():
+            same = torch.equal(getattr(layer.out, n).view(torch.int32), v.view(torch.int32))
+            if not same:
+                print(f"rank 0: {n} changed after the timeout", flush=True)
+            ok = ok and same
     dist.barrier()
     flag = torch.tensor([0 if ok else 1])
     dist.all_reduce(flag)

@@ -34,6 +34,8 @@ def main() -> int:
     ap.add_argument("--interval", type=int, default=1, help="re-placement interval (row f2)")
     ap.add_argument("--host-state", action="store_true", help="row f4: state in pinned host memory")
     ap.add_argument("--lazy", action="store_true", help="MOE_OPT_LAZY_REPLICATE (with --dedup)")
+    ap.add_argument("--edge", action="store_true",
+                    help="update-stage edge values: idle experts with zero grads, special grads and masters")
     ap.add_argument("--tokens", type=int, default=-1,
                     help="row f3: also run the token dispatch/combine with these flags (0 or 1)")
     args = ap.parse_args()
@@ -61,10 +63,15 @@ def main() -> int:
     seed = aseed if args.adhoc else configs.seed_for(wl.name)
     from oracle.dispatch import slot_capacity
     cap = slot_capacity(args.cf, wl.T, k, G * S) if args.cf > 0 else 0
+    from synth import edge
     layer = DecoupledExpertLayer(E, G, S, k, P, Tg, rank=rank, device=local, seed=seed,
                                  dedup=args.dedup, capacity=cap, policy=args.policy,
                                  replan_interval=args.interval, host_state=args.host_state,
-                                 lazy_replicate=args.lazy)
+                                 lazy_replicate=args.lazy, init_master=not args.edge)
+    if args.edge:   # edge masters for this rank's owner shard (synth/edge.py)
+        loc = np.arange(rank * Pg, (rank + 1) * Pg, dtype=np.uint64)
+        mb = np.stack([edge.edge_master_bits(seed, e, loc) for e in range(E)])
+        layer.master[0].copy_(torch.from_numpy(mb.view(np.float32).reshape(-1)))
     layer.connect()
     tx = None
     if args.tokens >= 0:
@@ -96,11 +103,16 @@ def main() -> int:
                                         np.arange(G) * Pg, np.arange(1, G + 1) * Pg - 1]))
     else:
         idx = np.arange(P)
+    master0 = None
+    if args.edge:
+        master0 = np.stack([edge.edge_master_bits(seed, e, idx.astype(np.uint64)) for e in range(E)]).view(np.float32)
     sim = ostep.OracleSim(E, G, S, P, seed, idx=idx, capacity=cap,
                           policy={0: "alg1", 1: "minmax", 2: "static"}[args.policy],
-                          replan_interval=args.interval)
+                          replan_interval=args.interval, master0=master0)
     idx_t = torch.from_numpy(idx).cuda()
-    if args.trace == "rotating-hot":
+    if args.edge:
+        tr = edge.idle_expert_trace(E, wl.T, k, args.iters, seed=seed)
+    elif args.trace == "rotating-hot":
         tr = traces.rotating_hot(E, wl.T, k, args.iters, seed=seed, hot_weight=4 if E < 16 else 16)
     else:
         tr = traces.make_trace(wl, iters=args.iters, seed=seed)
@@ -119,13 +131,27 @@ def main() -> int:
         expect(np.array_equal(w, sim.w_slot[rank * S:(rank + 1) * S]), f"iter {t}: slot weights")
 
     check_weights(-1)
+    gen = edge.edge_grad_bits if args.edge else hashgen.grad_bits
     for t, (ids, gates) in enumerate(tr):
-        synth_grads(layer.slot_g[0], seed, t, rank * S, S, P)
+        zs = set(edge.zero_slots(ids, E, sim.plan["slot_expert"]).tolist()) if args.edge else set()
+        if args.edge:
+            full = np.arange(P, dtype=np.uint64)
+            gb = np.stack([gen(seed, t, j, full) for j in range(rank * S, (rank + 1) * S)])
+            layer.slot_g[0].view(torch.int16).copy_(torch.from_numpy(gb.view(np.int16).reshape(-1)))
+            for j in zs:
+                if rank * S <= j < (rank + 1) * S:
+                    layer.slot_g[0][(j - rank * S) * P:(j - rank * S + 1) * P].zero_()
+        else:
+            synth_grads(layer.slot_g[0], seed, t, rank * S, S, P)
         my_ids = torch.from_numpy(traces.split_ranks(ids, G)[rank].copy()).cuda()
         my_gates = torch.from_numpy(traces.split_ranks(gates, G)[rank].copy()).cuda()
         layer.iterate(my_ids, my_gates, Tg)
-        res = sim.iterate(traces.split_ranks(ids, G), traces.split_ranks(gates, G),
-                          lambda j, t=t: hashgen.grad_bits(seed, t, j, idx.astype(np.uint64)))
+        def grad_of_slot(j, t=t):
+            if j in zs:
+                return np.zeros(idx.size, dtype=np.uint16)
+            return gen(seed, t, j, idx.astype(np.uint64))
+        with np.errstate(all="ignore"):
+            res = sim.iterate(traces.split_ranks(ids, G), traces.split_ranks(gates, G), grad_of_slot)
         layer.ctx.check()
         expect(layer.plan.replicas.tolist() == res["plan_next"]["replicas"].tolist(), f"iter {t}: plan")
         d = res["dispatch"]
@@ -149,7 +175,9 @@ def main() -> int:
         for nm, arr, want in (("master", layer.master, sim.master), ("m", layer.adam_m, sim.m),
                               ("v", layer.adam_v, sim.v)):
             got = arr[0].view(E, Pg)[:, li].cpu().numpy()
-            expect(np.array_equal(got.view(np.uint32), np.ascontiguousarray(want[:, sel]).view(np.uint32)),
+            w_ = np.ascontiguousarray(want[:, sel])
+            ng, nw = np.isnan(got), np.isnan(w_)   # NaN policy (reading A22): masks, not payloads
+            expect(np.array_equal(ng, nw) and np.array_equal(got.view(np.uint32)[~ng], w_.view(np.uint32)[~nw]),
                    f"iter {t}: {nm}")
         check_weights(t)
         if tx is not None:   # row f3 along this iteration's routing

@@ -11,6 +11,11 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.fixture(scope="module", autouse=True)
+def _built():
+    import __graft_entry__
+    __graft_entry__.build()
+    torch.cuda.set_device(0)
+
 
 def _plan_from_oracle(p, G, S):
     """The oracle's placement (replicas, first_slot, slot_expert) as a moe_plan_t for the layer."""
@@ -21,11 +26,6 @@ def _plan_from_oracle(p, G, S):
     pl.first_slot[:] = p["first_slot"]
     pl.slot_expert[:] = p["slot_expert"]
     return pl
-
-def _built():
-    import __graft_entry__
-    __graft_entry__.build()
-    torch.cuda.set_device(0)
 
 
 def _bits(rng, shape):

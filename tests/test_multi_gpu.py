@@ -49,6 +49,9 @@ def _torchrun(n: int, *args, timeout=600, script="mp_parity.py"):
     (4, "tiny", ["--adhoc", "13,4,2,1000,1344,12", "--dedup", "--tokens", "0"]),
     (4, "tiny", ["--adhoc", "3,3,3,404,96,13", "--policy", "1", "--interval", "2", "--iters", "5"]),
     (2, "tiny", ["--adhoc", "1,2,1,300,208,14", "--host-state"]),
+    # update-stage edge values over NVLink: zero-token experts, +-0, denormals, overflow, NaN
+    (2, "tiny-skew", ["--edge"]), (4, "medium", ["--edge", "--dedup", "--iters", "4"]),
+    (4, "tiny-skew", ["--edge", "--host-state", "--dedup"]),
 ], ids=lambda x: "".join(a.lstrip("-") for a in x) if isinstance(x, list) else str(x))
 def test_real_multi_gpu_parity(G, config, extra):
     if torch.cuda.device_count() < G:
