@@ -95,6 +95,40 @@ class ClockSampler:
                 "reasons": sorted(reasons)}
 
 
+class NvlinkCounters:
+    """NVML NVLink data counters (fields THROUGHPUT_DATA_TX/RX = 138/139, KiB, summed over
+    links) of this process's GPU, read around the timed region: a hardware cross-check of the
+    algorithmic NVLink bytes.  Silently unavailable if NVML or the fields are not."""
+    TX, RX, LINKS = 138, 139, 18
+
+    def __init__(self, device: int):
+        self.h = None
+        try:
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            uuid = str(torch.cuda.get_device_properties(device).uuid)
+            uuid = uuid if uuid.startswith("GPU-") else "GPU-" + uuid
+            self.h = pynvml.nvmlDeviceGetHandleByUUID(uuid)
+            self.nv = pynvml
+        except Exception as e:  # noqa: BLE001
+            self.err = f"NVML unavailable: {type(e).__name__}: {e}"[:160]
+
+    def read(self):
+        if self.h is None:
+            return None
+        try:
+            ids = [(self.TX, l) for l in range(self.LINKS)] + [(self.RX, l) for l in range(self.LINKS)]
+            vals = self.nv.nvmlDeviceGetFieldValues(self.h, ids)
+            tx = sum(v.value.ullVal for v in vals[:self.LINKS] if v.nvmlReturn == 0)
+            rx = sum(v.value.ullVal for v in vals[self.LINKS:] if v.nvmlReturn == 0)
+            ok = sum(1 for v in vals if v.nvmlReturn == 0)
+            return (tx * 1024, rx * 1024, ok)
+        except Exception as e:  # noqa: BLE001
+            self.err = f"NVML read failed: {type(e).__name__}: {e}"[:160]
+            return None
+
+
 def update_stage_bytes(fs_cur, fs_next, G: int, S: int, P: int, E: int, dedup: bool,
                        parts: bool = False, host_state: bool = False):
     """Algorithmic bytes of one update stage, from the two plans.
@@ -146,7 +180,8 @@ def update_stage_bytes(fs_cur, fs_next, G: int, S: int, P: int, E: int, dedup: b
     nvl = max(max(nin), max(nout))
     if parts:
         return {"stage_hbm": hbm, "nvl": nvl, "update_hbm": max(upd), "presum_hbm": max(pre),
-                "replicate_hbm": max(rep), "pcie_per_dir": 12 * E * Pg if host_state else 0}
+                "replicate_hbm": max(rep), "pcie_per_dir": 12 * E * Pg if host_state else 0,
+                "nvl_in": nin, "nvl_out": nout}
     return hbm, nvl
 
 
@@ -509,6 +544,8 @@ def gpu_arm(args, wl):
     layer.ctx.get_timing()                          # clear (timing hooks stay off while timed)
     barrier()
     step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
+    nvc = NvlinkCounters(local) if G > 1 else None
+    nv0 = nvc.read() if nvc else None
     start.record(stream)
     h0 = time.perf_counter()
     step_ev[0].record(stream)
@@ -519,6 +556,7 @@ def gpu_arm(args, wl):
     layer.sync_weights(stream)      # the last step's (possibly deferred) replication is timed too
     end.record(stream)
     barrier()
+    nv1 = nvc.read() if nvc else None
     clocks = clk.stop()
     layer.ctx.check()
     total_ms = start.elapsed_time(end)
@@ -628,7 +666,22 @@ def gpu_arm(args, wl):
     # algorithmic bytes, per timed iteration from the actual plans
     acc = [update_stage_bytes(fc, fn, G, S, wl.P, wl.E, args.dedup, parts=True,
                               host_state=args.host_state) for fc, fn in plans]
-    mean = {k: statistics.mean(a[k] for a in acc) for k in acc[0]}
+    mean = {k: statistics.mean(a[k] for a in acc) for k in acc[0] if not isinstance(acc[0][k], list)}
+    nvlink_hw = None
+    if nvc is not None:   # NVML data counters vs the algorithmic bytes, this rank, per step
+        if nv0 and nv1:
+            alg_out = statistics.mean(a["nvl_out"][rank] for a in acc)
+            alg_in = statistics.mean(a["nvl_in"][rank] for a in acc)
+            mine = {"tx_bytes_per_step": (nv1[0] - nv0[0]) / K, "rx_bytes_per_step": (nv1[1] - nv0[1]) / K,
+                    "alg_out_per_step": alg_out, "alg_in_per_step": alg_in, "links_read": nv1[2]}
+        else:
+            mine = {"error": getattr(nvc, "err", "no counters")}
+        allr = [None] * G
+        dist.all_gather_object(allr, mine)
+        nvlink_hw = {"per_rank": allr,
+                     "note": "NVML NVLINK_THROUGHPUT_DATA_TX/RX (KiB counters, all links) around the timed "
+                             "region / K vs update_stage_bytes' per-GPU algorithmic NVLink bytes (pulls + "
+                             "pushes of the update stage; dispatch count exchange not included)"}
     # roofline of the dominant kernel, k_update_tma alone (its own HBM and NVLink bytes)
     t_hbm_k = mean["update_hbm"] / (peak_hbm * 1e9)
     t_nvl = mean["nvl"] / (GUIDE_NVLINK_GBS * 1e9) if G > 1 else 0.0
@@ -710,6 +763,7 @@ def gpu_arm(args, wl):
                                   "de-dup k_presum + k_update_tma + k_replicate); max over ranks"},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(n_launch),
             "token_a2a": a2a,
+            "nvlink_counters": nvlink_hw,
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

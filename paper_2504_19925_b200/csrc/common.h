@@ -33,3 +33,6 @@ void *moe_hi_begin(moe_ctx *ctx, void *stream);          // stream for moe_step'
 int moe_hi_end(moe_ctx *ctx, void *hi, void *stream);    // join it back
 void moe_host_time(moe_ctx *ctx, int which, double ms);  // 0: wait for C_t, 1: planner, 2: launch
 void moe_ctx_schedule(const moe_ctx *ctx, int32_t *policy, int32_t *interval);  // ctx.cu
+int moe_update_early(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_adam_t *adam, void *stream,
+                     uint32_t *epoch);                                   // update.cu
+int moe_plan_publish(moe_ctx *ctx, const moe_plan_t *plan_next, uint32_t epoch);  // update.cu

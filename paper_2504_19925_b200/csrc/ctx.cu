@@ -100,6 +100,9 @@ void free_ctx(moe_ctx *c) {
   if (c->hs_in) cudaStreamDestroy(c->hs_in);
   if (c->hs_out) cudaStreamDestroy(c->hs_out);
   if (c->host_flag) cudaFreeHost((void *)c->host_flag);
+  cudaFree(c->plan_dev);
+  if (c->plan_pin) cudaFreeHost(c->plan_pin);
+  if (c->planq) cudaStreamDestroy(c->planq);
   for (auto *v : {&c->ev_pool, &c->ev_disp, &c->ev_upd, &c->ev_presum, &c->ev_repl, &c->ev_stage})
     for (auto &p : *v) {
       cudaEventDestroy(p.first);
@@ -215,6 +218,10 @@ extern "C" int moe_ctx_create(const moe_ctx_desc *d, moe_ctx **out) {
   chk(cudaMalloc(&c->err, sizeof(int32_t)));
   chk(cudaMalloc(&c->item_ctr, 3 * sizeof(unsigned long long)));
   chk(cudaMalloc(&c->scan_done, sizeof(uint32_t)));
+  chk(cudaMalloc(&c->plan_dev, sizeof(PlanDev)));
+  chk(cudaHostAlloc(&c->plan_pin, sizeof(PlanDev), cudaHostAllocDefault));
+  chk(cudaStreamCreateWithFlags(&c->planq, cudaStreamNonBlocking));
+  c->plan_epoch = 0;
   {
     void *hf = nullptr;
     chk(cudaHostAlloc(&hf, sizeof(uint32_t), cudaHostAllocMapped));
@@ -233,6 +240,8 @@ extern "C" int moe_ctx_create(const moe_ctx_desc *d, moe_ctx **out) {
     chk(cudaMemset(c->err, 0, sizeof(int32_t)));
     chk(cudaMemset(c->item_ctr, 0, 3 * sizeof(unsigned long long)));
     chk(cudaMemset(c->scan_done, 0, sizeof(uint32_t)));
+    chk(cudaMemset(c->plan_dev, 0, sizeof(PlanDev)));
+    memset(c->plan_pin, 0, sizeof(PlanDev));
     chk(cudaDeviceSynchronize());
   }
   if (e != cudaSuccess) {

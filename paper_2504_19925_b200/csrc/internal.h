@@ -34,6 +34,17 @@ struct SyncBuf {
   alignas(128) int32_t xcnt[2][MOE_MAX_G][MOE_MAX_E];  // per-rank expert counts, by epoch parity
 };
 
+// plan_{t+1} handed to the device by moe_step after the update kernel was enqueued
+// (double-buffered by the hand-off epoch's parity): the host writes it to a pinned mirror and
+// a copy engine moves it here, the epoch word last; the update and replicate kernels acquire
+// epoch[par] == their epoch before their first use of plan_{t+1} (the a5 stores).
+struct PlanDev {
+  alignas(16) int32_t fs[2][MOE_MAX_E + 4];  // first_slot [E+1]
+  alignas(16) uint8_t hfirst[2][MOE_MAX_E];  // first_slot[e] / S
+  alignas(128) uint32_t epoch[2];
+  uint32_t pad[30];
+};
+
 // Per-expert dispatch parameters computed by the scan kernel, read by the scatter kernel.
 struct ExpertInfo {
   int32_t base;     // global rank of this rank's first pair of the expert
@@ -66,6 +77,11 @@ struct moe_ctx {
   bool connected;
   uint32_t disp_epoch, upd_epoch;
   int32_t sched_policy, sched_interval;  // moe_ctx_set_schedule (row f2)
+  // moe_step's early update launch: plan_{t+1} reaches the device after the kernel is queued
+  moe::PlanDev *plan_dev;   // device
+  moe::PlanDev *plan_pin;   // pinned host mirror (the copy-engine source)
+  cudaStream_t planq;       // copy stream of the hand-off
+  uint32_t plan_epoch;
 
   // caller buffers, per local rank
   std::vector<void *> slot_w, slot_g;

@@ -25,9 +25,20 @@ extern "C" int moe_step(moe_ctx *ctx, const int32_t *topk_ids, const float *gate
   st = moe_hi_end(ctx, ds, stream);
   if (st) return moe_step_abort(ctx, st);
   using clk = std::chrono::steady_clock;
+  // a3 + a4 + a5 enqueued NOW, before plan_{t+1} exists: reduce and Adam need only plan_t; the
+  // kernel acquires plan_{t+1} from device memory just before its first a5 store, so the host
+  // planner and the hand-off copy overlap the dispatch tail and the update's start instead of
+  // sitting between the two kernels (0 = early path unavailable: launch after planning)
+  const auto tl0 = clk::now();
+  uint32_t pend = 0;
+  st = moe_update_early(ctx, plan_cur, adam, stream, &pend);
+  if (st) return moe_step_abort(ctx, st);
   const auto t0 = clk::now();
   st = moe_ctx_wait_counts(ctx);  // C_t on the host
-  if (st) return moe_step_abort(ctx, st);
+  if (st) {
+    if (pend) moe_plan_publish(ctx, nullptr, pend);  // release the queued kernel (places nothing)
+    return moe_step_abort(ctx, st);
+  }
   const auto t1 = clk::now();
   if (policy == MOE_PLAN_SCHEDULED) {  // the library's schedule decides (row f2, reading B3)
     int32_t sp = 0, si = 1;
@@ -39,11 +50,18 @@ extern "C" int moe_step(moe_ctx *ctx, const int32_t *topk_ids, const float *gate
     st = moe_plan_ex(out->counts_host, plan_cur->E, plan_cur->G, plan_cur->S, policy, plan_next,
                      nullptr);  // a1 -> plan_{t+1}
   }
-  if (st) return moe_step_abort(ctx, st);
+  if (st) {
+    if (pend) moe_plan_publish(ctx, nullptr, pend);
+    return moe_step_abort(ctx, st);
+  }
   const auto t2 = clk::now();
-  st = moe_update(ctx, plan_cur, plan_next, adam, stream);  // a3 + a4 + a5
+  if (pend) {
+    st = moe_plan_publish(ctx, plan_next, pend);  // a1's result to the queued a5 stores
+  } else {
+    st = moe_update(ctx, plan_cur, plan_next, adam, stream);  // a3 + a4 + a5
+  }
   moe_host_time(ctx, 0, std::chrono::duration<double, std::milli>(t1 - t0).count());
   moe_host_time(ctx, 1, std::chrono::duration<double, std::milli>(t2 - t1).count());
-  moe_host_time(ctx, 2, std::chrono::duration<double, std::milli>(clk::now() - t2).count());
+  moe_host_time(ctx, 2, std::chrono::duration<double, std::milli>((clk::now() - t2) + (t0 - tl0)).count());
   return st;
 }

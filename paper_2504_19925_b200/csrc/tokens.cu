@@ -85,7 +85,13 @@ struct TokArgs {
   int32_t *err;
 };
 
+// Both kernels are launched with programmatic dependent launch (PDL): their launch and CTA
+// rasterisation overlap the tail of the previous kernel in the stream.  griddepcontrol.wait
+// (before any global access, and before the arrive flag, whose meaning is "my earlier
+// kernels are complete") waits for that kernel's completion and memory flush.
 __device__ __forceinline__ void arrive_and_wait(const TokArgs &a) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (a.rank < 0 || a.G == 1) return;
   if (blockIdx.x == 0 && threadIdx.x < a.G) st_release_sys(&a.psync[threadIdx.x]->arrive[a.rank], a.epoch);
   if (threadIdx.x < a.G) wait_flag(&a.psync[a.rank]->arrive[threadIdx.x], a.epoch, a.err);
@@ -272,7 +278,7 @@ __device__ __forceinline__ void prefetch_row_l2(const uint4 *row, int64_t dv) {
 // pointers), fp32 adds in ascending j (reading C2).  k > 32 falls back to per-pair loads.
 // While token t is summed, the bulk-copy engine already prefetches the k rows of the warp's
 // next token into L2 (one cp.async.bulk.prefetch per row), so its loads are L2 hits.
-template <int U>
+template <int U, bool kFull>  // kFull: dv % (32 U) == 0, no per-vector bounds checks
 __global__ void __launch_bounds__(kThreads, 4) k_tok_combine(TokArgs a) {
   arrive_and_wait(a);
   const int lane = threadIdx.x & 31;
@@ -342,8 +348,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_tok_combine(TokArgs a) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int64_t c = c0 + u * 32 + lane;
-          if (r0 && c < a.dv) y0[u] = ldg_nc(r0 + c);  // rows are final before the arrive flags
-          if (r1 && c < a.dv) y1[u] = ldg_nc(r1 + c);
+          if (r0 && (kFull || c < a.dv)) y0[u] = ldg_nc(r0 + c);  // rows are final before the arrive flags
+          if (r1 && (kFull || c < a.dv)) y1[u] = ldg_nc(r1 + c);
         }
         if (r0) tok_accum(a, acc, y0, g0);
         if (r1) tok_accum(a, acc, y1, g1);
@@ -351,7 +357,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_tok_combine(TokArgs a) {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int64_t c = c0 + u * 32 + lane;
-        if (c < a.dv) {
+        if (kFull || c < a.dv) {
           uint4 o;
           o.x = pack2(acc[u][0], acc[u][1]);
           o.y = pack2(acc[u][2], acc[u][3]);
@@ -450,7 +456,7 @@ extern "C" int moe_tokx_create(moe_ctx *ctx, int64_t d, int64_t rows, void *cons
     return fail(MOE_ERR_CUDA, "moe_tokx_create: cannot allocate the sync buffer");
   }
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tok_combine<kCombU>, kThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tok_combine<kCombU, false>, kThreads, 0);
   x->blocks = ctx->num_sms * (per_sm > 0 ? per_sm : 1);
   if (ctx->rank < 0) {
     for (int h = 0; h < ctx->G; ++h) {
@@ -530,6 +536,20 @@ extern "C" int moe_tokx_connect(moe_tokx *x, const void *all) {
   return MOE_OK;
 }
 
+template <typename K>
+cudaError_t launch_tok(K kern, unsigned blocks, cudaStream_t s, const TokArgs &a) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(kThreads);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
 extern "C" int moe_token_dispatch(moe_tokx *x, const void *const *src, int64_t T, const float *gates,
                                   const moe_dispatch_out *out, int32_t flags, void *stream) {
   if (!x || !src) return fail(MOE_ERR_INVALID, "moe_token_dispatch: NULL argument");
@@ -546,8 +566,7 @@ extern "C" int moe_token_dispatch(moe_tokx *x, const void *const *src, int64_t T
   cudaStream_t s = (cudaStream_t)stream;
   const bool sync = c->rank >= 0 && c->G > 1;
   a.epoch = sync ? ++x->arrive_epoch : 0;
-  k_tok_dispatch<<<x->blocks, kThreads, 0, s>>>(a);
-  MOE_CUDA_TRY(cudaGetLastError());
+  MOE_CUDA_TRY(launch_tok(k_tok_dispatch, x->blocks, s, a));
   if (sync) {
     // the done flags reuse the arrive epoch (one dispatch per arrive increment is enough:
     // done[] is written only by dispatches, and epochs only grow)
@@ -572,7 +591,9 @@ extern "C" int moe_token_combine(moe_tokx *x, void *const *dst, int64_t T, const
   MOE_CUDA_TRY(cudaSetDevice(c->device));
   const bool sync = c->rank >= 0 && c->G > 1;
   a.epoch = sync ? ++x->arrive_epoch : 0;
-  k_tok_combine<kCombU><<<x->blocks, kThreads, 0, (cudaStream_t)stream>>>(a);
-  MOE_CUDA_TRY(cudaGetLastError());
+  if (x->dv % (32 * kCombU) == 0)
+    MOE_CUDA_TRY(launch_tok(k_tok_combine<kCombU, true>, x->blocks, (cudaStream_t)stream, a));
+  else
+    MOE_CUDA_TRY(launch_tok(k_tok_combine<kCombU, false>, x->blocks, (cudaStream_t)stream, a));
   return MOE_OK;
 }

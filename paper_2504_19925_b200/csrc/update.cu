@@ -60,6 +60,13 @@ struct UpdArgs {
   int32_t dedup;
   int8_t pq[MOE_MAX_E][MOE_MAX_G];  // row of expert e's fp32 partial on GPU h under plan_cur, or -1
   const float *presum[MOE_MAX_G];   // per GPU h: fp32 [nq_max][P]
+  // moe_step's early launch: plan_{t+1} (fs_next / h_first_next) is read from device memory
+  // once *pflag == pepoch (set by a copy engine after the host planner ran); nullptr: the
+  // plan is in the parameters above
+  const int32_t *fsn_dev;
+  const uint8_t *hfn_dev;
+  const uint32_t *pflag;
+  uint32_t pepoch;
   // development trace (env MOE_KTRACE): globaltimer stamps folded with atomics, printed by the
   // CTA that completes barrier-out.  [0] min start [1] max start [2] max barrier-in done
   // [3] min consumer done [4] max consumer done
@@ -123,11 +130,10 @@ __device__ __forceinline__ void st_stream8(uint16_t *p, const uint2 &v) {
 }
 
 // a5 for k_update_tma's split mapping: 4 bf16 at element gi and (if has_b) 4 at gi + kChunk/2,
-// into the same slots as place_to.
-__device__ __forceinline__ void place_split(const UpdArgs &a, int e, int owner, int64_t gi,
+// into the same slots as place_to; plan_{t+1}'s run of e is [n0, n1), starting on GPU h.
+__device__ __forceinline__ void place_split(const UpdArgs &a, int n0, int n1, int h, int owner, int64_t gi,
                                             const uint2 &wa, const uint2 &wbv, bool has_b) {
-  const int n0 = a.fs_next[e], n1 = a.fs_next[e + 1];
-  int h = a.h_first_next[e], l = n0 - h * a.S;
+  int l = n0 - h * a.S;
   for (int j = n0; j < n1; ++j) {
     if (!a.dedup || h == owner || j == n0 || l == 0) {
       uint16_t *dst = a.wbase[h] + (int64_t)l * a.P + gi;
@@ -139,6 +145,27 @@ __device__ __forceinline__ void place_split(const UpdArgs &a, int e, int owner, 
       ++h;
     }
   }
+}
+
+// Early launch: wait (one lane per warp) until the host's plan_{t+1} has landed in device
+// memory.  False on timeout (the error bit is raised; the caller then places nothing).
+__device__ __forceinline__ bool plan_flag_wait(const uint32_t *p, uint32_t epoch, int32_t *err) {
+  const uint64_t t0 = globaltimer();
+  for (;;) {
+    const uint32_t f = ld_acquire_sys(p);
+    if (f == epoch) return true;
+    if (f == (epoch | 0x80000000u)) return false;  // poisoned: the host step failed
+    if (globaltimer() - t0 > kSpinTimeoutNs) {
+      atomicOr(err, kErrTimeout);
+      return false;
+    }
+    __nanosleep(128);
+  }
+}
+__device__ __forceinline__ bool wait_plan(const UpdArgs &a, int lane) {
+  int ok = 1;
+  if (lane == 0) ok = plan_flag_wait(a.pflag, a.pepoch, a.err) ? 1 : 0;
+  return __shfl_sync(0xffffffffu, ok, 0) != 0;
 }
 
 // a4: Adam on 8 elements, reading A15 op order, IEEE fp32 RN per op, bf16 RNE out.
@@ -457,6 +484,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_update_tma(const __grid_cons
   constexpr int H = kChunk / 2;
   const int tid = threadIdx.x;
   uint32_t si = 0, gi_ = 0;
+  int plan_state = 0;  // early launch: 0 not yet seen, 1 plan_{t+1} available, 2 timed out
   for (;;) {
     const int s = si % kStateSlots;
     mbar_wait(st_full + s, (si / kStateSlots) & 1);
@@ -535,6 +563,8 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_update_tma(const __grid_cons
       have_tot = true;
       ja = jb;
     }
+    // early launch: the first item's place needs plan_{t+1} (whole warp, before any lane exits)
+    if (a.pflag && plan_state == 0) plan_state = wait_plan(a, lane) ? 1 : 2;
     if (!act_a) continue;  // (act_b implies act_a)
     uint4 wb;
     adam8(a, tot, a.scale[e], w, m, v, wb);                              // a4
@@ -550,7 +580,18 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_update_tma(const __grid_cons
       pm[H / 4] = make_float4(m[4], m[5], m[6], m[7]);
       pv[H / 4] = make_float4(v[4], v[5], v[6], v[7]);
     }
-    place_split(a, e, o, (int64_t)o * a.Pg + loc, make_uint2(wb.x, wb.y), make_uint2(wb.z, wb.w),
+    int n0, n1, hn;
+    if (a.pflag) {  // early launch: plan_{t+1} from device memory (acquired above)
+      if (plan_state != 1) continue;
+      n0 = __ldcg(a.fsn_dev + e);
+      n1 = __ldcg(a.fsn_dev + e + 1);
+      hn = __ldcg(reinterpret_cast<const int8_t *>(a.hfn_dev) + e) & 0xff;
+    } else {
+      n0 = a.fs_next[e];
+      n1 = a.fs_next[e + 1];
+      hn = a.h_first_next[e];
+    }
+    place_split(a, n0, n1, hn, o, (int64_t)o * a.Pg + loc, make_uint2(wb.x, wb.y), make_uint2(wb.z, wb.w),
                 act_b);                                                    // a5
   }
 
@@ -651,6 +692,9 @@ struct ReplArgs {
   int64_t P, Pg;
   int32_t fs[MOE_MAX_E + 1];  // plan_next
   uint16_t *w[MOE_MAX_G];     // local rank v: bf16 slot weights [S][P]
+  const int32_t *fs_dev;      // early launch: plan_next in device memory (valid iff *pflag == pepoch)
+  const uint32_t *pflag;
+  uint32_t pepoch;
 };
 
 // One CTA row per local slot; only the FIRST slot of an expert with local duplicates works: it
@@ -660,14 +704,19 @@ __global__ void __launch_bounds__(kThreads) k_replicate(const __grid_constant__ 
   const int v = blockIdx.y / a.S, l = blockIdx.y % a.S;
   const int h = a.o_begin + v;
   const int j = h * a.S + l;
+  const int32_t *fs = a.fs;
+  if (a.pflag) {  // ordered after the update kernel, which acquired the plan: check, no wait
+    if (ld_acquire_sys(a.pflag) != a.pepoch) return;
+    fs = a.fs_dev;
+  }
   int lo = 0, hi = a.E - 1;  // expert of global slot j: largest e with fs[e] <= j
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
-    if (a.fs[mid] <= j) lo = mid;
+    if (fs[mid] <= j) lo = mid;
     else hi = mid - 1;
   }
-  const int j0 = max(a.fs[lo], h * a.S);      // GPU h's first slot of that expert
-  const int jb = min(a.fs[lo + 1], (h + 1) * a.S);
+  const int j0 = max(fs[lo], h * a.S);      // GPU h's first slot of that expert
+  const int jb = min(fs[lo + 1], (h + 1) * a.S);
   if (j != j0 || jb - j0 < 2) return;
   const int ndup = jb - j0 - 1;
   const uint16_t *src = a.w[v] + (int64_t)l * a.P;
@@ -774,8 +823,10 @@ int build_presum(moe_ctx *ctx, const moe_plan_t *plan_cur, int8_t (&pq)[MOE_MAX_
 }
 
 // Shared launcher of moe_update (place_only = 0) and moe_place (place_only = 1).
+// pend_epoch != 0 (moe_step's early launch): plan_next is NULL -- the kernels read plan_{t+1}
+// from ctx->plan_dev once its epoch word reaches pend_epoch (moe_plan_publish).
 int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *plan_next,
-                  const moe_adam_t *adam, int place_only, void *stream) {
+                  const moe_adam_t *adam, int place_only, void *stream, uint32_t pend_epoch = 0) {
   if (ctx->rank >= 0 && ctx->G > 1 && !ctx->connected)
     return fail(MOE_ERR_INVALID, "moe_update/moe_place: real-mode context not connected");
   MOE_CUDA_TRY(cudaSetDevice(ctx->device));
@@ -824,13 +875,20 @@ int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *pl
       }
     }
   }
+  const int par = (int)(pend_epoch & 1u);
   for (int e = 0; e <= ctx->E; ++e) {
     a.fs_cur[e] = plan_cur->first_slot[e];
-    a.fs_next[e] = plan_next->first_slot[e];
+    if (!pend_epoch) a.fs_next[e] = plan_next->first_slot[e];
   }
   for (int e = 0; e < ctx->E; ++e) {
     a.h_first_cur[e] = (uint8_t)(plan_cur->first_slot[e] / ctx->S);
-    a.h_first_next[e] = (uint8_t)(plan_next->first_slot[e] / ctx->S);
+    if (!pend_epoch) a.h_first_next[e] = (uint8_t)(plan_next->first_slot[e] / ctx->S);
+  }
+  if (pend_epoch) {
+    a.fsn_dev = ctx->plan_dev->fs[par];
+    a.hfn_dev = ctx->plan_dev->hfirst[par];
+    a.pflag = &ctx->plan_dev->epoch[par];
+    a.pepoch = pend_epoch;
   }
   for (int h = 0; h < ctx->G; ++h) {
     a.gbase[h] = (const uint16_t *)ctx->peer_slot_g[h];
@@ -991,14 +1049,21 @@ int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *pl
     ra.o_begin = a.o_begin;
     ra.P = ctx->P;
     ra.Pg = ctx->Pg;
-    for (int e = 0; e <= ctx->E; ++e) ra.fs[e] = plan_next->first_slot[e];
     int nsrc = 0;  // experts with local duplicates (one source each)
-    for (int v = 0; v < ctx->n_local; ++v) {
-      ra.w[v] = (uint16_t *)ctx->slot_w[v];
-      const int h = a.o_begin + v;
-      for (int e = 0; e < ctx->E; ++e) {
-        const int ja = std::max(ra.fs[e], h * ctx->S), jb = std::min(ra.fs[e + 1], (h + 1) * ctx->S);
-        if (jb - ja > 1) ++nsrc;
+    for (int v = 0; v < ctx->n_local; ++v) ra.w[v] = (uint16_t *)ctx->slot_w[v];
+    if (pend_epoch) {  // plan_next not known yet: launch for any, sized as if every slot were one
+      ra.fs_dev = ctx->plan_dev->fs[par];
+      ra.pflag = &ctx->plan_dev->epoch[par];
+      ra.pepoch = pend_epoch;
+      nsrc = std::max(1, ctx->n_local * ctx->S / 2);
+    } else {
+      for (int e = 0; e <= ctx->E; ++e) ra.fs[e] = plan_next->first_slot[e];
+      for (int v = 0; v < ctx->n_local; ++v) {
+        const int h = a.o_begin + v;
+        for (int e = 0; e < ctx->E; ++e) {
+          const int ja = std::max(ra.fs[e], h * ctx->S), jb = std::min(ra.fs[e + 1], (h + 1) * ctx->S);
+          if (jb - ja > 1) ++nsrc;
+        }
       }
     }
     if (nsrc > 0) {
@@ -1074,6 +1139,48 @@ int moe_presum_prelaunch(moe_ctx *ctx, const moe_plan_t *plan_cur, void *stream)
 int moe_step_abort(moe_ctx *ctx, int status) {
   ctx->presum_ready = false;
   return status;
+}
+
+// moe_step's early update launch (plan_{t+1} pending on the device).  Only with the bulk-copy
+// kernel (the register-staged one reads the plan from its parameters).  Returns the hand-off
+// epoch (> 0) in *epoch, or 0 if the early path does not apply (the caller then launches the
+// update after planning, as moe_update does).
+int moe_update_early(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_adam_t *adam, void *stream,
+                     uint32_t *epoch) {
+  *epoch = 0;
+  if (!ctx || !adam || (ctx->update_kernel == 0 && !ctx->dedup) || !ctx->plan_dev) return MOE_OK;
+  int st = moe_validate_plan(ctx, plan_cur, "moe_step(plan_cur)");
+  if (st) return st;
+  if (adam->step < 1) return fail(MOE_ERR_INVALID, "moe_update: Adam step must be >= 1");
+  if (adam->scale_mode < 0 || adam->scale_mode > 2 || (adam->scale_mode == 2 && !adam->scale))
+    return fail(MOE_ERR_INVALID, "moe_update: bad scale_mode / scale");
+  uint32_t ep = (ctx->plan_epoch + 1) & 0x7fffffffu;  // bit 31 marks a poisoned hand-off
+  if (ep == 0) ep = 1;
+  st = launch_update(ctx, plan_cur, nullptr, adam, 0, stream, ep);
+  if (st) return st;
+  ctx->plan_epoch = ep;
+  *epoch = ep;
+  return MOE_OK;
+}
+
+// Hands plan_{t+1} to an early-launched update: pinned mirror -> device by a copy engine, the
+// epoch word last (poison = the epoch with bit 31 set: the kernels place nothing, raise no
+// wait, and the step reports the host-side error).
+int moe_plan_publish(moe_ctx *ctx, const moe_plan_t *plan_next, uint32_t epoch) {
+  const int par = (int)(epoch & 1u);
+  PlanDev *hp = ctx->plan_pin;
+  if (plan_next) {
+    for (int e = 0; e <= ctx->E; ++e) hp->fs[par][e] = plan_next->first_slot[e];
+    for (int e = 0; e < ctx->E; ++e) hp->hfirst[par][e] = (uint8_t)(plan_next->first_slot[e] / ctx->S);
+    MOE_CUDA_TRY(cudaMemcpyAsync(ctx->plan_dev->fs[par], hp->fs[par], sizeof(int32_t) * (ctx->E + 1),
+                                 cudaMemcpyHostToDevice, ctx->planq));
+    MOE_CUDA_TRY(cudaMemcpyAsync(ctx->plan_dev->hfirst[par], hp->hfirst[par], ctx->E, cudaMemcpyHostToDevice,
+                                 ctx->planq));
+  }
+  hp->epoch[par] = plan_next ? epoch : (epoch | 0x80000000u);
+  MOE_CUDA_TRY(cudaMemcpyAsync(&ctx->plan_dev->epoch[par], &hp->epoch[par], sizeof(uint32_t),
+                               cudaMemcpyHostToDevice, ctx->planq));
+  return MOE_OK;
 }
 
 extern "C" int moe_place(moe_ctx *ctx, const moe_plan_t *plan, void *stream) {

@@ -13,10 +13,28 @@ Argument marshalling and ordering only; every stage runs in libmoedc.
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
 from . import api
+
+
+def _gpu_local_cpus(device: int):
+    """CPUs NVML reports as close to `device` (its NUMA node), or None."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        uuid = str(torch.cuda.get_device_properties(device).uuid)
+        h = pynvml.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, 16)
+        cpus = {64 * i + b for i, w in enumerate(words) for b in range(64) if (int(w) >> b) & 1}
+        allowed = os.sched_getaffinity(0)
+        cpus &= allowed
+        return cpus or None
+    except Exception:  # noqa: BLE001
+        return None
 
 
 class DecoupledExpertLayer:
@@ -52,9 +70,17 @@ class DecoupledExpertLayer:
         self.slot_w = [torch.empty(S * P, dtype=torch.bfloat16, device=dev) for _ in range(n)]
         self.slot_g = [torch.zeros(S * P, dtype=torch.bfloat16, device=dev) for _ in range(n)]
         if host_state:   # row f4: pinned host DRAM, device-accessible through UVA
+            # allocate (and first-touch) the pinned state from the GPU's own NUMA node: the
+            # calling thread runs on the CPUs NVML lists as local to the device meanwhile
+            local_cpus = _gpu_local_cpus(device)
+            prev_aff = os.sched_getaffinity(0) if local_cpus else None
+            if local_cpus:
+                os.sched_setaffinity(0, local_cpus)
+            self.numa_local_cpus = len(local_cpus) if local_cpus else 0
+
             def state(zero):
                 t = torch.empty(E * self.Pg, dtype=torch.float32, pin_memory=True)
-                return t.zero_() if zero else t
+                return t.zero_() if zero else t.fill_(0.0)
         else:
             def state(zero):
                 f = torch.zeros if zero else torch.empty
@@ -62,6 +88,8 @@ class DecoupledExpertLayer:
         self.master = [state(False) for _ in range(n)]
         self.adam_m = [state(True) for _ in range(n)]
         self.adam_v = [state(True) for _ in range(n)]
+        if host_state and prev_aff:
+            os.sched_setaffinity(0, prev_aff)
         self.host_state = host_state
         opts = ((api.MOE_OPT_DEDUP if dedup else 0) | (api.MOE_OPT_HOST_STATE if host_state else 0) |
                 (api.MOE_OPT_LAZY_REPLICATE if lazy_replicate else 0))
