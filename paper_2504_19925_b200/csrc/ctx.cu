@@ -100,6 +100,9 @@ void free_ctx(moe_ctx *c) {
   if (c->hs_in) cudaStreamDestroy(c->hs_in);
   if (c->hs_out) cudaStreamDestroy(c->hs_out);
   if (c->host_flag) cudaFreeHost((void *)c->host_flag);
+  for (auto &row : c->tl_ev)
+    for (auto &ev : row)
+      if (ev) cudaEventDestroy(ev);
   cudaFree(c->plan_dev);
   if (c->plan_pin) cudaFreeHost(c->plan_pin);
   if (c->planq) cudaStreamDestroy(c->planq);
@@ -222,6 +225,7 @@ extern "C" int moe_ctx_create(const moe_ctx_desc *d, moe_ctx **out) {
   chk(cudaHostAlloc(&c->plan_pin, sizeof(PlanDev), cudaHostAllocDefault));
   chk(cudaStreamCreateWithFlags(&c->planq, cudaStreamNonBlocking));
   c->plan_epoch = 0;
+  c->tl_on = getenv("MOE_TIMELINE") != nullptr;  // development trace only
   {
     void *hf = nullptr;
     chk(cudaHostAlloc(&hf, sizeof(uint32_t), cudaHostAllocMapped));
@@ -544,4 +548,36 @@ extern "C" int moe_ctx_check(moe_ctx *ctx, void *stream) {
     return fail(MOE_ERR_DATA, "invalid topk ids (outside [0,E) or repeated within a token)");
   }
   return MOE_OK;
+}
+
+// MOE_TIMELINE: called by moe_step (after its wait for C_t, when the previous step's device
+// work is done or nearly) -- prints the previous step's stage timeline, ms from its start.
+void moe_timeline_step(moe_ctx *c, void *s) {
+  if (!c->tl_on) return;
+  const int prev = c->tl_par ^ 1;
+  if (c->tl_set[prev][TL_STEP]) {
+    cudaEvent_t e0 = c->tl_ev[prev][TL_STEP];
+    static const char *nm[TL_N] = {"step", "presum", "", "dispatch", "", "update", "", "replicate", ""};
+    char buf[512];
+    int n = snprintf(buf, sizeof(buf), "TIMELINE rank %d step %lld:", c->rank, (long long)(c->tl_step - 1));
+    for (int p = TL_PRESUM_B; p < TL_N; p += 2) {
+      if (!c->tl_set[prev][p] || !c->tl_set[prev][p + 1]) continue;
+      float a = 0, b = 0;
+      cudaEventSynchronize(c->tl_ev[prev][p + 1]);
+      cudaEventElapsedTime(&a, e0, c->tl_ev[prev][p]);
+      cudaEventElapsedTime(&b, e0, c->tl_ev[prev][p + 1]);
+      n += snprintf(buf + n, sizeof(buf) - n, " %s %+.1f..%+.1f us |", nm[p], 1e3 * a, 1e3 * b);
+    }
+    fprintf(stderr, "%s\n", buf);
+  }
+  for (int p = 0; p < TL_N; ++p) c->tl_set[prev][p] = false;
+  (void)s;
+}
+
+void moe_timeline_begin(moe_ctx *c, void *s) {
+  if (!c->tl_on) return;
+  c->tl_par ^= 1;
+  for (int p = 0; p < TL_N; ++p) c->tl_set[c->tl_par][p] = false;
+  ++c->tl_step;
+  tl_mark(c, TL_STEP, (cudaStream_t)s);
 }

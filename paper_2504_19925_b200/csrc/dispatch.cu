@@ -682,6 +682,7 @@ extern "C" int moe_dispatch(moe_ctx *ctx, const int32_t *topk_ids, const float *
   ha.counts_host = counts_host_dev;
   ha.host_flag = ctx->host_flag_dev;
   const auto tev = timing_begin(ctx, s);
+  tl_mark(ctx, TL_DISP_B, s);
   k_hist<<<dim3(nb, ctx->n_local), kThreads, 0, s>>>(ha);
   MOE_CUDA_TRY(cudaGetLastError());
 
@@ -735,5 +736,6 @@ extern "C" int moe_dispatch(moe_ctx *ctx, const int32_t *topk_ids, const float *
     MOE_CUDA_TRY(launch_pdl(k_scatter, dim3(nb, ctx->n_local), s, ca, scatter_smem((int)tile, ctx->G * ctx->S),
                             kSThreads));
   timing_end(ctx->ev_disp, tev, s);
+  tl_mark(ctx, TL_DISP_E, s);
   return MOE_OK;
 }

@@ -132,6 +132,13 @@ struct moe_ctx {
   uint32_t *host_flag_dev;       // its device (UVA) alias
   bool counts_pending;
   unsigned long long *ktrace;    // MOE_KTRACE development trace scratch (lazily allocated)
+  // MOE_TIMELINE development trace: CUDA events at stage boundaries on their own streams,
+  // double-buffered by step; moe_step prints the previous step's timeline (stderr)
+  bool tl_on;
+  int tl_par;
+  int64_t tl_step;
+  cudaEvent_t tl_ev[2][12];
+  bool tl_set[2][12];
 
   std::map<std::string, void *> opened;  // IPC handle bytes -> mapped base (dedup)
 
@@ -143,6 +150,13 @@ struct moe_ctx {
 };
 
 namespace moe {
+enum TlPoint { TL_STEP = 0, TL_PRESUM_B, TL_PRESUM_E, TL_DISP_B, TL_DISP_E, TL_UPD_B, TL_UPD_E, TL_REPL_B,
+               TL_REPL_E, TL_N };
+inline void tl_mark(moe_ctx *c, int pt, cudaStream_t s) {
+  if (!c->tl_on) return;
+  if (!c->tl_ev[c->tl_par][pt] && cudaEventCreate(&c->tl_ev[c->tl_par][pt]) != cudaSuccess) return;
+  if (cudaEventRecord(c->tl_ev[c->tl_par][pt], s) == cudaSuccess) c->tl_set[c->tl_par][pt] = true;
+}
 // Record the start of a timed region (returns the pair to close), or {nullptr, nullptr}.
 inline std::pair<cudaEvent_t, cudaEvent_t> timing_begin(moe_ctx *c, cudaStream_t s) {
   if (!c->timing) return {nullptr, nullptr};

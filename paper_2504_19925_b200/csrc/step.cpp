@@ -15,6 +15,7 @@ extern "C" int moe_step(moe_ctx *ctx, const int32_t *topk_ids, const float *gate
   if (!ctx || !out || !plan_cur || !plan_next || !adam)
     return moe::fail(MOE_ERR_INVALID, "moe_step: NULL argument");
   if (!out->counts_host) return moe::fail(MOE_ERR_INVALID, "moe_step: out->counts_host is required");
+  moe_timeline_begin(ctx, stream);
   // de-dup partials (a3's first level) need only plan_t and the grads: start them now on a
   // low-priority side stream, overlapping the dispatch and the host planner
   int st = moe_presum_prelaunch(ctx, plan_cur, stream);
@@ -40,6 +41,7 @@ extern "C" int moe_step(moe_ctx *ctx, const int32_t *topk_ids, const float *gate
     return moe_step_abort(ctx, st);
   }
   const auto t1 = clk::now();
+  moe_timeline_step(ctx, stream);
   if (policy == MOE_PLAN_SCHEDULED) {  // the library's schedule decides (row f2, reading B3)
     int32_t sp = 0, si = 1;
     moe_ctx_schedule(ctx, &sp, &si);

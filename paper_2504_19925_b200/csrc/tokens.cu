@@ -249,7 +249,8 @@ __device__ __forceinline__ void tok_accum(const TokArgs &a, float (&acc)[U][8], 
 // 32 x kCombU vectors, loading two rows' chunks before accumulating either (shuffled
 // pointers), fp32 adds in ascending j (reading C2).  k > 32 falls back to per-pair loads.
 // Lane j < k's row pointer and gate for pair j of global token index tk (nullptr: dropped).
-__device__ __forceinline__ void comb_src(const TokArgs &a, uint32_t tk, int lane, const uint4 *&row, float &g) {
+__device__ __forceinline__ void comb_src(const TokArgs &a, uint32_t tk, int lane, const uint4 *&row, float &g,
+                                         bool *local) {
   row = nullptr;
   g = 1.f;
   if (lane >= a.k || lane >= 32) return;
@@ -265,6 +266,7 @@ __device__ __forceinline__ void comb_src(const TokArgs &a, uint32_t tk, int lane
   const uint32_t h = (uint32_t)s / (uint32_t)a.S;
   row = a.xb[h] + ((int64_t)((uint32_t)s - h * (uint32_t)a.S) * a.rows + off) * a.dv;
   if (a.gate) g = __ldg(a.gates + p);
+  if (local) *local = a.rank < 0 || (int)h == a.rank;
 }
 
 // Bulk-copy engine prefetch of a whole row (local or peer HBM) into this GPU's L2.
@@ -277,7 +279,8 @@ __device__ __forceinline__ void prefetch_row_l2(const uint4 *row, int64_t dv) {
 // 32 x kCombU vectors, loading two rows' chunks before accumulating either (shuffled
 // pointers), fp32 adds in ascending j (reading C2).  k > 32 falls back to per-pair loads.
 // While token t is summed, the bulk-copy engine already prefetches the k rows of the warp's
-// next token into L2 (one cp.async.bulk.prefetch per row), so its loads are L2 hits.
+// next token into L2 (one cp.async.bulk.prefetch per row), so its loads are L2 hits -- local
+// rows only: prefetching a peer's rows over NVLink made the N = 4 combine 50x slower.
 template <int U, bool kFull>  // kFull: dv % (32 U) == 0, no per-vector bounds checks
 __global__ void __launch_bounds__(kThreads, 4) k_tok_combine(TokArgs a) {
   arrive_and_wait(a);
@@ -287,7 +290,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_tok_combine(TokArgs a) {
   uint32_t tok = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
   const uint4 *nx_row = nullptr;
   float nx_g = 1.f;
-  if (tok < ntok) comb_src(a, tok, lane, nx_row, nx_g);
+  if (tok < ntok) comb_src(a, tok, lane, nx_row, nx_g, nullptr);
   for (; tok < ntok; tok += warps) {
     const uint32_t v = tok / (uint32_t)a.T;
     const uint32_t t = tok - v * (uint32_t)a.T;
@@ -295,8 +298,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_tok_combine(TokArgs a) {
     const uint4 *my_row = nx_row;
     const float my_g = nx_g;
     if (tok + warps < ntok) {
-      comb_src(a, tok + warps, lane, nx_row, nx_g);
-      if (nx_row) prefetch_row_l2(nx_row, a.dv);
+      bool local = true;
+      comb_src(a, tok + warps, lane, nx_row, nx_g, &local);
+      if (nx_row && local) prefetch_row_l2(nx_row, a.dv);  // peer rows: no (measured 50x slower)
     }
     uint4 *dst = a.dst[v] + (int64_t)t * a.dv;
     for (int64_t c0 = 0; c0 < a.dv; c0 += 32 * U) {

@@ -165,7 +165,9 @@ __device__ __forceinline__ bool plan_flag_wait(const uint32_t *p, uint32_t epoch
 __device__ __forceinline__ bool wait_plan(const UpdArgs &a, int lane) {
   int ok = 1;
   if (lane == 0) ok = plan_flag_wait(a.pflag, a.pepoch, a.err) ? 1 : 0;
-  return __shfl_sync(0xffffffffu, ok, 0) != 0;
+  ok = __shfl_sync(0xffffffffu, ok, 0);
+  __threadfence();  // once per warp: every lane's later plan loads are ordered after the acquire
+  return ok != 0;
 }
 
 // a4: Adam on 8 elements, reading A15 op order, IEEE fp32 RN per op, bf16 RNE out.
@@ -979,6 +981,7 @@ int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *pl
     }
     return MOE_OK;
   };
+  if (!place_only) tl_mark(ctx, TL_UPD_B, s);
   if (!(ctx->host_state && !place_only)) {
     const int st = run_kernel(a);
     if (st) return st;
@@ -1037,6 +1040,7 @@ int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *pl
     MOE_CUDA_TRY(cudaEventRecord(ctx->hs_ev_end, ctx->hs_out));  // the state is home again
     MOE_CUDA_TRY(cudaStreamWaitEvent(s, ctx->hs_ev_end, 0));
   }
+  if (!place_only) tl_mark(ctx, TL_UPD_E, s);
   if (multi && !tma) {  // barrier-out: every push into this GPU's slots has landed
     ba.which = 1;
     k_barrier<<<1, 32, 0, s>>>(ba);
@@ -1076,9 +1080,11 @@ int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *pl
         rs = ctx->repl;
       }
       const auto rev = timing_begin(ctx, rs);
+      tl_mark(ctx, TL_REPL_B, rs);
       k_replicate<<<dim3(gx, ctx->n_local * ctx->S), kThreads, 0, rs>>>(ra);
       MOE_CUDA_TRY(cudaGetLastError());
       timing_end(ctx->ev_repl, rev, rs);
+      tl_mark(ctx, TL_REPL_E, rs);
       if (ctx->lazy_repl) {
         MOE_CUDA_TRY(cudaEventRecord(ctx->ev_repl_done, rs));
         ctx->repl_pending = true;
@@ -1126,9 +1132,11 @@ int moe_presum_prelaunch(moe_ctx *ctx, const moe_plan_t *plan_cur, void *stream)
     // stream, take every SM slot a retiring presum CTA frees
     const int64_t grid = std::min<int64_t>((int64_t)pa.nq_total * pa.nchunks, (int64_t)1 << 30);
     const auto pev = timing_begin(ctx, ctx->side);
+    tl_mark(ctx, TL_PRESUM_B, ctx->side);
     k_presum<<<(unsigned)grid, kThreads, 0, ctx->side>>>(pa);
     MOE_CUDA_TRY(cudaGetLastError());
     timing_end(ctx->ev_presum, pev, ctx->side);
+    tl_mark(ctx, TL_PRESUM_E, ctx->side);
   }
   MOE_CUDA_TRY(cudaEventRecord(ctx->ev_presum_done, ctx->side));
   ctx->presum_fs.assign(plan_cur->first_slot, plan_cur->first_slot + ctx->E + 1);
