@@ -34,7 +34,7 @@ int moe_hi_end(moe_ctx *ctx, void *hi, void *stream);    // join it back
 void moe_host_time(moe_ctx *ctx, int which, double ms);  // 0: wait for C_t, 1: planner, 2: launch
 void moe_ctx_schedule(const moe_ctx *ctx, int32_t *policy, int32_t *interval);  // ctx.cu
 int moe_update_early(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_adam_t *adam, void *stream,
-                     uint32_t *epoch);                                   // update.cu
+                     uint32_t *epoch, bool pdl_after_dispatch);          // update.cu
 int moe_plan_publish(moe_ctx *ctx, const moe_plan_t *plan_next, uint32_t epoch);  // update.cu
 void moe_timeline_begin(moe_ctx *ctx, void *stream);  // ctx.cu (MOE_TIMELINE development trace)
 void moe_timeline_step(moe_ctx *ctx, void *stream);

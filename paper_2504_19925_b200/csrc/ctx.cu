@@ -105,7 +105,6 @@ void free_ctx(moe_ctx *c) {
       if (ev) cudaEventDestroy(ev);
   cudaFree(c->plan_dev);
   if (c->plan_pin) cudaFreeHost(c->plan_pin);
-  if (c->planq) cudaStreamDestroy(c->planq);
   for (auto *v : {&c->ev_pool, &c->ev_disp, &c->ev_upd, &c->ev_presum, &c->ev_repl, &c->ev_stage})
     for (auto &p : *v) {
       cudaEventDestroy(p.first);
@@ -222,8 +221,12 @@ extern "C" int moe_ctx_create(const moe_ctx_desc *d, moe_ctx **out) {
   chk(cudaMalloc(&c->item_ctr, 3 * sizeof(unsigned long long)));
   chk(cudaMalloc(&c->scan_done, sizeof(uint32_t)));
   chk(cudaMalloc(&c->plan_dev, sizeof(PlanDev)));
-  chk(cudaHostAlloc(&c->plan_pin, sizeof(PlanDev), cudaHostAllocDefault));
-  chk(cudaStreamCreateWithFlags(&c->planq, cudaStreamNonBlocking));
+  chk(cudaHostAlloc(&c->plan_pin, sizeof(PlanDev), cudaHostAllocMapped));
+  if (c->plan_pin) {
+    void *dp = nullptr;
+    chk(cudaHostGetDevicePointer(&dp, c->plan_pin, 0));
+    c->plan_pin_dev = (PlanDev *)dp;
+  }
   c->plan_epoch = 0;
   c->tl_on = getenv("MOE_TIMELINE") != nullptr;  // development trace only
   {

@@ -386,6 +386,7 @@ __global__ void __launch_bounds__(kSThreads) k_scatter(const __grid_constant__ S
   const int64_t off_v = (int64_t)v * a.npairs;
   const int64_t tbase = (int64_t)b * a.tile;
   const int n = (int)min((int64_t)a.tile, a.npairs - tbase);
+  pdl_trigger();  // moe_step's update kernel (PDL) may take the SMs this grid's CTAs free
   {  // stage the tile's ids and gates (inputs, not produced by k_scan): independent, coalesced
     const int32_t *ip = a.ids + off_v + tbase;
     const int32_t *gp = reinterpret_cast<const int32_t *>(a.gates) + off_v + tbase;

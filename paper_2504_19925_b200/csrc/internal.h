@@ -35,9 +35,12 @@ struct SyncBuf {
 };
 
 // plan_{t+1} handed to the device by moe_step after the update kernel was enqueued
-// (double-buffered by the hand-off epoch's parity): the host writes it to a pinned mirror and
-// a copy engine moves it here, the epoch word last; the update and replicate kernels acquire
-// epoch[par] == their epoch before their first use of plan_{t+1} (the a5 stores).
+// (double-buffered by the hand-off epoch's parity).  The host writes it into a mapped pinned
+// mirror, the epoch word last; an otherwise idle producer lane of the update kernel's CTA 0
+// polls that word over PCIe, copies the plan into the device copy and releases the device
+// epoch; every consumer warp acquires the device epoch before its first a5 store.  No CUDA
+// call and no extra stream on the host side (a copy-engine hand-off on a library stream could
+// share a hardware queue with the spinning kernel and deadlock until the timeout).
 struct PlanDev {
   alignas(16) int32_t fs[2][MOE_MAX_E + 4];  // first_slot [E+1]
   alignas(16) uint8_t hfirst[2][MOE_MAX_E];  // first_slot[e] / S
@@ -79,8 +82,8 @@ struct moe_ctx {
   int32_t sched_policy, sched_interval;  // moe_ctx_set_schedule (row f2)
   // moe_step's early update launch: plan_{t+1} reaches the device after the kernel is queued
   moe::PlanDev *plan_dev;   // device
-  moe::PlanDev *plan_pin;   // pinned host mirror (the copy-engine source)
-  cudaStream_t planq;       // copy stream of the hand-off
+  moe::PlanDev *plan_pin;   // mapped pinned host mirror (written by the host planner)
+  moe::PlanDev *plan_pin_dev;  // its device (UVA) alias
   uint32_t plan_epoch;
 
   // caller buffers, per local rank

@@ -32,7 +32,7 @@ extern "C" int moe_step(moe_ctx *ctx, const int32_t *topk_ids, const float *gate
   // sitting between the two kernels (0 = early path unavailable: launch after planning)
   const auto tl0 = clk::now();
   uint32_t pend = 0;
-  st = moe_update_early(ctx, plan_cur, adam, stream, &pend);
+  st = moe_update_early(ctx, plan_cur, adam, stream, &pend, ds == stream);
   if (st) return moe_step_abort(ctx, st);
   const auto t0 = clk::now();
   st = moe_ctx_wait_counts(ctx);  // C_t on the host

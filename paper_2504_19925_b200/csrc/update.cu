@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 
 #include "internal.h"
@@ -67,6 +68,10 @@ struct UpdArgs {
   const uint8_t *hfn_dev;
   const uint32_t *pflag;
   uint32_t pepoch;
+  // ... moved there from the mapped pinned host mirror by producer lanes 1-31 of CTA 0
+  const int32_t *fsn_host;
+  const uint8_t *hfn_host;
+  const uint32_t *pflag_host;
   // development trace (env MOE_KTRACE): globaltimer stamps folded with atomics, printed by the
   // CTA that completes barrier-out.  [0] min start [1] max start [2] max barrier-in done
   // [3] min consumer done [4] max consumer done
@@ -149,6 +154,43 @@ __device__ __forceinline__ void place_split(const UpdArgs &a, int n0, int n1, in
 
 // Early launch: wait (one lane per warp) until the host's plan_{t+1} has landed in device
 // memory.  False on timeout (the error bit is raised; the caller then places nothing).
+// Producer lanes 1-31 of CTA 0 (idle otherwise): wait for the host's epoch word in the mapped
+// pinned mirror (lane 1 polls over PCIe), copy plan_{t+1} into device memory and release the
+// device epoch (a poisoned or timed-out hand-off is forwarded as the poisoned epoch).  If the
+// device epoch is already set (a later window launch of the same step) nothing is done.
+__device__ __forceinline__ void plan_handoff(const UpdArgs &a, int lane) {
+  const unsigned m = 0xfffffffeu;  // lanes 1-31
+  uint32_t f = 0;
+  if (lane == 1) {
+    f = ld_acquire_sys(a.pflag);
+    if (f != a.pepoch && f != (a.pepoch | 0x80000000u)) {
+      const uint64_t t0 = globaltimer();
+      for (;;) {
+        f = ld_acquire_sys(a.pflag_host);
+        if (f == a.pepoch || f == (a.pepoch | 0x80000000u)) break;
+        if (globaltimer() - t0 > kSpinTimeoutNs) {
+          atomicOr(a.err, kErrTimeout);
+          f = a.pepoch | 0x80000000u;
+          break;
+        }
+        __nanosleep(256);
+      }
+    } else {
+      f = 0;  // already handed off
+    }
+  }
+  f = __shfl_sync(m, f, 1);
+  if (f == 0) return;
+  if (f == a.pepoch) {
+    int32_t *fs = const_cast<int32_t *>(a.fsn_dev);
+    uint8_t *hf = const_cast<uint8_t *>(a.hfn_dev);
+    for (int i = lane - 1; i <= a.E; i += 31) fs[i] = a.fsn_host[i];
+    for (int i = lane - 1; i < a.E; i += 31) hf[i] = a.hfn_host[i];
+  }
+  __syncwarp(m);
+  if (lane == 1) st_release_sys(const_cast<uint32_t *>(a.pflag), f);  // after the warp's copies
+}
+
 __device__ __forceinline__ bool plan_flag_wait(const uint32_t *p, uint32_t epoch, int32_t *err) {
   const uint64_t t0 = globaltimer();
   for (;;) {
@@ -407,7 +449,10 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_update_tma(const __grid_cons
   }
 
   if (warp == kConsumerWarps) {  // ---------------- producer ----------------
-    if (lane != 0) return;
+    if (lane != 0) {
+      if (a.pflag && blockIdx.x == 0) plan_handoff(a, lane);  // early launch: move plan_{t+1}
+      return;
+    }
     if (a.fused_barrier)
       for (int h = 0; h < a.G; ++h) wait_flag(&a.sync_local->upd_in[h], a.epoch, a.err);
     if (a.ktrace) atomicMax(a.ktrace + 2, globaltimer());
@@ -828,7 +873,8 @@ int build_presum(moe_ctx *ctx, const moe_plan_t *plan_cur, int8_t (&pq)[MOE_MAX_
 // pend_epoch != 0 (moe_step's early launch): plan_next is NULL -- the kernels read plan_{t+1}
 // from ctx->plan_dev once its epoch word reaches pend_epoch (moe_plan_publish).
 int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *plan_next,
-                  const moe_adam_t *adam, int place_only, void *stream, uint32_t pend_epoch = 0) {
+                  const moe_adam_t *adam, int place_only, void *stream, uint32_t pend_epoch = 0,
+                  bool pdl_after_dispatch = false) {
   if (ctx->rank >= 0 && ctx->G > 1 && !ctx->connected)
     return fail(MOE_ERR_INVALID, "moe_update/moe_place: real-mode context not connected");
   MOE_CUDA_TRY(cudaSetDevice(ctx->device));
@@ -891,6 +937,9 @@ int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *pl
     a.hfn_dev = ctx->plan_dev->hfirst[par];
     a.pflag = &ctx->plan_dev->epoch[par];
     a.pepoch = pend_epoch;
+    a.fsn_host = ctx->plan_pin_dev->fs[par];
+    a.hfn_host = ctx->plan_pin_dev->hfirst[par];
+    a.pflag_host = &ctx->plan_pin_dev->epoch[par];
   }
   for (int h = 0; h < ctx->G; ++h) {
     a.gbase[h] = (const uint16_t *)ctx->peer_slot_g[h];
@@ -974,8 +1023,25 @@ int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *pl
       const int64_t grid = std::min<int64_t>(items, (int64_t)ctx->num_sms * 2);
       if (grid > 0) {
         const auto tev = timing_begin(ctx, s);
-        k_update_tma<kGradSlots><<<(unsigned)grid, kTmaThreads, tma_smem<kGradSlots>(), s>>>(ka);
-        MOE_CUDA_TRY(cudaGetLastError());
+        if (pdl_after_dispatch && !ka.ktrace && !tev.first) {
+          // moe_step, dispatch on this stream: programmatic dependent launch -- the update reads
+          // nothing the scatter writes (plan_{t+1} arrives by its own flag), so its CTAs take
+          // the SMs the scatter's retiring CTAs free, without griddepcontrol.wait
+          cudaLaunchConfig_t cfg{};
+          cfg.gridDim = dim3((unsigned)grid);
+          cfg.blockDim = dim3(kTmaThreads);
+          cfg.dynamicSmemBytes = tma_smem<kGradSlots>();
+          cfg.stream = s;
+          cudaLaunchAttribute attr[1];
+          attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+          attr[0].val.programmaticStreamSerializationAllowed = 1;
+          cfg.attrs = attr;
+          cfg.numAttrs = 1;
+          MOE_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_update_tma<kGradSlots>, ka));
+        } else {
+          k_update_tma<kGradSlots><<<(unsigned)grid, kTmaThreads, tma_smem<kGradSlots>(), s>>>(ka);
+          MOE_CUDA_TRY(cudaGetLastError());
+        }
         timing_end(ctx->ev_upd, tev, s);
       }
     }
@@ -1154,9 +1220,10 @@ int moe_step_abort(moe_ctx *ctx, int status) {
 // epoch (> 0) in *epoch, or 0 if the early path does not apply (the caller then launches the
 // update after planning, as moe_update does).
 int moe_update_early(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_adam_t *adam, void *stream,
-                     uint32_t *epoch) {
+                     uint32_t *epoch, bool pdl) {
   *epoch = 0;
-  if (!ctx || !adam || (ctx->update_kernel == 0 && !ctx->dedup) || !ctx->plan_dev) return MOE_OK;
+  if (!ctx || !adam || (ctx->update_kernel == 0 && !ctx->dedup) || !ctx->plan_dev || !ctx->plan_pin_dev)
+    return MOE_OK;
   int st = moe_validate_plan(ctx, plan_cur, "moe_step(plan_cur)");
   if (st) return st;
   if (adam->step < 1) return fail(MOE_ERR_INVALID, "moe_update: Adam step must be >= 1");
@@ -1164,30 +1231,29 @@ int moe_update_early(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_adam_t 
     return fail(MOE_ERR_INVALID, "moe_update: bad scale_mode / scale");
   uint32_t ep = (ctx->plan_epoch + 1) & 0x7fffffffu;  // bit 31 marks a poisoned hand-off
   if (ep == 0) ep = 1;
-  st = launch_update(ctx, plan_cur, nullptr, adam, 0, stream, ep);
+  // PDL only for the single-launch case (no host-state windows; without de-dup nothing else is
+  // launched between the scatter and the update)
+  st = launch_update(ctx, plan_cur, nullptr, adam, 0, stream, ep, pdl && !ctx->host_state && !ctx->dedup &&
+                                                                       !ctx->timing && !ctx->tl_on);
   if (st) return st;
   ctx->plan_epoch = ep;
   *epoch = ep;
   return MOE_OK;
 }
 
-// Hands plan_{t+1} to an early-launched update: pinned mirror -> device by a copy engine, the
-// epoch word last (poison = the epoch with bit 31 set: the kernels place nothing, raise no
-// wait, and the step reports the host-side error).
+// Hands plan_{t+1} to an early-launched update: plain host stores into the mapped pinned
+// mirror, the epoch word last (release); the kernel moves it to device memory.  Poison = the
+// epoch with bit 31 set: the kernels place nothing and the step reports the host-side error.
 int moe_plan_publish(moe_ctx *ctx, const moe_plan_t *plan_next, uint32_t epoch) {
   const int par = (int)(epoch & 1u);
   PlanDev *hp = ctx->plan_pin;
   if (plan_next) {
     for (int e = 0; e <= ctx->E; ++e) hp->fs[par][e] = plan_next->first_slot[e];
     for (int e = 0; e < ctx->E; ++e) hp->hfirst[par][e] = (uint8_t)(plan_next->first_slot[e] / ctx->S);
-    MOE_CUDA_TRY(cudaMemcpyAsync(ctx->plan_dev->fs[par], hp->fs[par], sizeof(int32_t) * (ctx->E + 1),
-                                 cudaMemcpyHostToDevice, ctx->planq));
-    MOE_CUDA_TRY(cudaMemcpyAsync(ctx->plan_dev->hfirst[par], hp->hfirst[par], ctx->E, cudaMemcpyHostToDevice,
-                                 ctx->planq));
   }
-  hp->epoch[par] = plan_next ? epoch : (epoch | 0x80000000u);
-  MOE_CUDA_TRY(cudaMemcpyAsync(&ctx->plan_dev->epoch[par], &hp->epoch[par], sizeof(uint32_t),
-                               cudaMemcpyHostToDevice, ctx->planq));
+  std::atomic_thread_fence(std::memory_order_release);
+  reinterpret_cast<std::atomic<uint32_t> *>(&hp->epoch[par])
+      ->store(plan_next ? epoch : (epoch | 0x80000000u), std::memory_order_release);
   return MOE_OK;
 }
 
