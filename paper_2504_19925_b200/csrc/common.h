@@ -38,3 +38,4 @@ int moe_update_early(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_adam_t 
 int moe_plan_publish(moe_ctx *ctx, const moe_plan_t *plan_next, uint32_t epoch);  // update.cu
 void moe_timeline_begin(moe_ctx *ctx, void *stream);  // ctx.cu (MOE_TIMELINE development trace)
 void moe_timeline_step(moe_ctx *ctx, void *stream);
+int ctx_rank(const moe_ctx *ctx);  // ctx.cu

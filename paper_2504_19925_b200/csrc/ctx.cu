@@ -584,3 +584,5 @@ void moe_timeline_begin(moe_ctx *c, void *s) {
   ++c->tl_step;
   tl_mark(c, TL_STEP, (cudaStream_t)s);
 }
+
+int ctx_rank(const moe_ctx *c) { return c->rank; }

@@ -6,6 +6,8 @@
 // place (a3-a5).  The host planner runs while the device still executes the scatter kernel,
 // and the update is enqueued as soon as the plan exists.
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 
 #include "common.h"
 
@@ -62,6 +64,12 @@ extern "C" int moe_step(moe_ctx *ctx, const int32_t *topk_ids, const float *gate
   } else {
     st = moe_update(ctx, plan_cur, plan_next, adam, stream);  // a3 + a4 + a5
   }
+  if (getenv("MOE_TIMELINE"))  // development trace: host phases of this step (us)
+    fprintf(stderr, "HOSTSTEP rank %d: early-launch %.1f | wait C_t %.1f | plan %.1f | publish/launch %.1f\n",
+            ctx_rank(ctx), std::chrono::duration<double, std::micro>(t0 - tl0).count(),
+            std::chrono::duration<double, std::micro>(t1 - t0).count(),
+            std::chrono::duration<double, std::micro>(t2 - t1).count(),
+            std::chrono::duration<double, std::micro>(clk::now() - t2).count());
   moe_host_time(ctx, 0, std::chrono::duration<double, std::milli>(t1 - t0).count());
   moe_host_time(ctx, 1, std::chrono::duration<double, std::milli>(t2 - t1).count());
   moe_host_time(ctx, 2, std::chrono::duration<double, std::milli>((clk::now() - t2) + (t0 - tl0)).count());

@@ -542,6 +542,15 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_update_tma(const __grid_cons
     const int e = (int)(rem % a.E);
     const int64_t c = a.c_lo + rem / a.E;
     const int64_t loc = c * kChunk + (int64_t)tid * 4;  // group A; group B at loc + H
+    // early launch, plan already acquired: fetch this item's run of plan_{t+1} now, so the
+    // loads overlap the reduce instead of preceding the stores
+    const bool pre_ok = a.pflag && plan_state == 1;
+    int pn0 = 0, pn1 = 0, phn = 0;
+    if (pre_ok) {
+      pn0 = a.fsn_dev[e];
+      pn1 = a.fsn_dev[e + 1];
+      phn = a.hfn_dev[e];
+    }
     const bool act_a = loc < a.Pg, act_b = loc + H < a.Pg;  // (P/G) % 8 == 0: groups are whole
     float w[8], m[8], v[8];
     {
@@ -628,11 +637,16 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_update_tma(const __grid_cons
       pv[H / 4] = make_float4(v[4], v[5], v[6], v[7]);
     }
     int n0, n1, hn;
-    if (a.pflag) {  // early launch: plan_{t+1} from device memory (acquired above)
-      if (plan_state != 1) continue;
-      n0 = __ldcg(a.fsn_dev + e);
-      n1 = __ldcg(a.fsn_dev + e + 1);
-      hn = __ldcg(reinterpret_cast<const int8_t *>(a.hfn_dev) + e) & 0xff;
+    if (a.pflag) {  // early launch: plan_{t+1} from device memory (acquired above; the
+      if (plan_state != 1) continue;  // acquire invalidated L1, so plain loads are fresh and
+      if (!pre_ok) {                   // later items hit L1)
+        pn0 = a.fsn_dev[e];
+        pn1 = a.fsn_dev[e + 1];
+        phn = a.hfn_dev[e];
+      }
+      n0 = pn0;
+      n1 = pn1;
+      hn = phn;
     } else {
       n0 = a.fs_next[e];
       n1 = a.fs_next[e + 1];
@@ -1222,7 +1236,9 @@ int moe_step_abort(moe_ctx *ctx, int status) {
 int moe_update_early(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_adam_t *adam, void *stream,
                      uint32_t *epoch, bool pdl) {
   *epoch = 0;
-  if (!ctx || !adam || (ctx->update_kernel == 0 && !ctx->dedup) || !ctx->plan_dev || !ctx->plan_pin_dev)
+  static const bool disabled = getenv("MOE_NO_EARLY") != nullptr;  // A/B switch
+  if (disabled || !ctx || !adam || (ctx->update_kernel == 0 && !ctx->dedup) || !ctx->plan_dev ||
+      !ctx->plan_pin_dev)
     return MOE_OK;
   int st = moe_validate_plan(ctx, plan_cur, "moe_step(plan_cur)");
   if (st) return st;
