@@ -103,6 +103,8 @@ class NvlinkCounters:
 
     def __init__(self, device: int):
         self.h = None
+        self.device = device
+        self.src = "NVML field values"
         try:
             import pynvml
             import torch
@@ -115,6 +117,13 @@ class NvlinkCounters:
             self.err = f"NVML unavailable: {type(e).__name__}: {e}"[:160]
 
     def read(self):
+        r = self._read_nvml()
+        if r is None or r[2] == 0:   # fields unsupported: nvidia-smi's per-link data counters
+            r2 = self._read_smi()
+            return r2 if r2 is not None else r
+        return r
+
+    def _read_nvml(self):
         if self.h is None:
             return None
         try:
@@ -126,6 +135,26 @@ class NvlinkCounters:
             return (tx * 1024, rx * 1024, ok)
         except Exception as e:  # noqa: BLE001
             self.err = f"NVML read failed: {type(e).__name__}: {e}"[:160]
+            return None
+
+    def _read_smi(self):
+        import re
+        import torch
+        try:
+            uuid = str(torch.cuda.get_device_properties(self.device).uuid)
+            uuid = uuid if uuid.startswith("GPU-") else "GPU-" + uuid
+            out = subprocess.run(["nvidia-smi", "nvlink", "-gt", "d", "-i", uuid], capture_output=True,
+                                 text=True, timeout=20).stdout
+            tx = sum(int(x) for x in re.findall(r"Data Tx:\s*(\d+)\s*KiB", out))
+            rx = sum(int(x) for x in re.findall(r"Data Rx:\s*(\d+)\s*KiB", out))
+            n = len(re.findall(r"Data Tx:", out))
+            if n == 0:
+                self.err = ("nvidia-smi nvlink -gt d: no counters: " + out.strip()[:120]) if out else "no output"
+                return None
+            self.src = "nvidia-smi nvlink -gt d"
+            return (tx * 1024, rx * 1024, n)
+        except Exception as e:  # noqa: BLE001
+            self.err = f"nvidia-smi nvlink failed: {type(e).__name__}: {e}"[:160]
             return None
 
 
@@ -538,14 +567,16 @@ def gpu_arm(args, wl):
     K = args.steps
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clk = ClockSampler(local)
+    # NVLink counters read before the last barrier (NVML init / nvidia-smi take ms: done inside
+    # the barrier-bracketed region it would desynchronise the ranks' first timed step)
+    nvc = NvlinkCounters(local) if G > 1 else None
+    nv0 = nvc.read() if nvc else None
     barrier()
     clk.start()
     time.sleep(0.3)
     layer.ctx.get_timing()                          # clear (timing hooks stay off while timed)
     barrier()
     step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
-    nvc = NvlinkCounters(local) if G > 1 else None
-    nv0 = nvc.read() if nvc else None
     start.record(stream)
     h0 = time.perf_counter()
     step_ev[0].record(stream)
@@ -673,7 +704,8 @@ def gpu_arm(args, wl):
             alg_out = statistics.mean(a["nvl_out"][rank] for a in acc)
             alg_in = statistics.mean(a["nvl_in"][rank] for a in acc)
             mine = {"tx_bytes_per_step": (nv1[0] - nv0[0]) / K, "rx_bytes_per_step": (nv1[1] - nv0[1]) / K,
-                    "alg_out_per_step": alg_out, "alg_in_per_step": alg_in, "links_read": nv1[2]}
+                    "alg_out_per_step": alg_out, "alg_in_per_step": alg_in, "links_read": nv1[2],
+                    "source": nvc.src}
         else:
             mine = {"error": getattr(nvc, "err", "no counters")}
         allr = [None] * G

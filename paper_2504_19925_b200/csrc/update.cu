@@ -1210,7 +1210,12 @@ int moe_presum_prelaunch(moe_ctx *ctx, const moe_plan_t *plan_cur, void *stream)
   if (pa.nq_total > 0) {
     // one item per CTA (non-persistent): the dispatch CTAs, launched on the higher-priority
     // stream, take every SM slot a retiring presum CTA frees
-    const int64_t grid = std::min<int64_t>((int64_t)pa.nq_total * pa.nchunks, (int64_t)1 << 30);
+    // persistent, 2 CTAs per SM (grid-stride over items): leaves each SM the registers and
+    // shared memory for the concurrent high-priority dispatch CTAs; the earlier one-item-per-CTA
+    // grid (tens of thousands of short CTAs) was CTA-launch bound.  MOE_PRESUM_GRID=items: A/B
+    static const bool per_item = getenv("MOE_PRESUM_GRID") != nullptr;
+    const int64_t grid = std::min<int64_t>((int64_t)pa.nq_total * pa.nchunks,
+                                           per_item ? ((int64_t)1 << 30) : (int64_t)ctx->num_sms * 2);
     const auto pev = timing_begin(ctx, ctx->side);
     tl_mark(ctx, TL_PRESUM_B, ctx->side);
     k_presum<<<(unsigned)grid, kThreads, 0, ctx->side>>>(pa);
