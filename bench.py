@@ -593,6 +593,7 @@ def gpu_arm(args, wl):
     total_ms = start.elapsed_time(end)
     # stage breakdown: the same K steps again with the library's CUDA-event hooks on (their
     # event records sit on the host's critical path, so `value` is timed without them)
+    barrier()   # ranks leave the clock sampler's teardown at different times
     layer.ctx.set_timing(True)
     for i in range(K):
         step(args.warmup + K + i)

@@ -288,6 +288,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_tok_combine(TokArgs a) {
   const uint32_t warps = gridDim.x * (kThreads / 32);
   const uint32_t ntok = (uint32_t)(a.T * a.n_local);  // < 2^31 (moe_ctx_create)
   uint32_t tok = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  const bool pf_ok = (int64_t)a.k * a.dv * 16 <= 8192;
   const uint4 *nx_row = nullptr;
   float nx_g = 1.f;
   if (tok < ntok) comb_src(a, tok, lane, nx_row, nx_g, nullptr);
@@ -300,7 +301,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_tok_combine(TokArgs a) {
     if (tok + warps < ntok) {
       bool local = true;
       comb_src(a, tok + warps, lane, nx_row, nx_g, &local);
-      if (nx_row && local) prefetch_row_l2(nx_row, a.dv);  // peer rows: no (measured 50x slower)
+      // peer rows: no (measured 50x slower at N = 4); and only while a token's k rows are small
+      // enough that 32 warps/SM of look-ahead stay far below the L2 (Qwen3: 32 KB/token, 0.61 of
+      // HBM with the prefetch -- it thrashed)
+      if (nx_row && local && pf_ok) prefetch_row_l2(nx_row, a.dv);
     }
     uint4 *dst = a.dst[v] + (int64_t)t * a.dv;
     for (int64_t c0 = 0; c0 < a.dv; c0 += 32 * U) {

@@ -1196,7 +1196,8 @@ extern "C" int moe_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_pl
 // highest-priority stream.  moe_update then waits on its event instead of launching it.
 int moe_presum_prelaunch(moe_ctx *ctx, const moe_plan_t *plan_cur, void *stream) {
   ctx->presum_ready = false;
-  if (!ctx->dedup) return MOE_OK;
+  static const bool serial = getenv("MOE_PRESUM_SERIAL") != nullptr;  // A/B: pre-sum after the dispatch
+  if (!ctx->dedup || serial) return MOE_OK;
   int st = moe_validate_plan(ctx, plan_cur, "moe_step(plan_cur)");
   if (st) return st;
   MOE_CUDA_TRY(cudaSetDevice(ctx->device));
