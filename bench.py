@@ -116,6 +116,48 @@ class NvlinkCounters:
         except Exception as e:  # noqa: BLE001
             self.err = f"NVML unavailable: {type(e).__name__}: {e}"[:160]
 
+    def gpm_start(self):
+        """NVML GPM sample (Hopper+): NVLINK_TOTAL_TX/RX_PER_SEC averaged between two samples."""
+        self.g1 = None
+        if self.h is None:
+            return
+        try:
+            self.g1 = self.nv.nvmlGpmSampleAlloc()
+            self.nv.nvmlGpmSampleGet(self.h, self.g1)
+            self.gt1 = time.perf_counter()
+        except Exception as e:  # noqa: BLE001
+            self.g1 = None
+            self.gpm_err = f"GPM unavailable: {type(e).__name__}: {e}"[:160]
+
+    def gpm_stop(self):
+        if getattr(self, "g1", None) is None:
+            return {"error": getattr(self, "gpm_err", "no GPM sample")}
+        try:
+            nv = self.nv
+            g2 = nv.nvmlGpmSampleAlloc()
+            nv.nvmlGpmSampleGet(self.h, g2)
+            dt = time.perf_counter() - self.gt1
+            mg = nv.c_nvmlGpmMetricsGet_t()
+            mg.version = nv.NVML_GPM_METRICS_GET_VERSION
+            mg.numMetrics = 2
+            mg.sample1 = self.g1
+            mg.sample2 = g2
+            mg.metrics[0].metricId = nv.NVML_GPM_METRIC_NVLINK_TOTAL_TX_PER_SEC
+            mg.metrics[1].metricId = nv.NVML_GPM_METRIC_NVLINK_TOTAL_RX_PER_SEC
+            nv.nvmlGpmMetricsGet(mg)
+            out = {"interval_s": dt}
+            for i, k in enumerate(("tx", "rx")):
+                m = mg.metrics[i]
+                unit = getattr(m.metricInfo, "unit", b"")
+                unit = unit.decode() if isinstance(unit, bytes) else str(unit)
+                out[k + "_per_sec"] = m.value if m.nvmlReturn == 0 else None
+                out[k + "_unit"] = unit
+            nv.nvmlGpmSampleFree(self.g1)
+            nv.nvmlGpmSampleFree(g2)
+            return out
+        except Exception as e:  # noqa: BLE001
+            return {"error": f"GPM read failed: {type(e).__name__}: {e}"[:160]}
+
     def read(self):
         r = self._read_nvml()
         if r is None or r[2] == 0:   # fields unsupported: nvidia-smi's per-link data counters
@@ -571,6 +613,8 @@ def gpu_arm(args, wl):
     # the barrier-bracketed region it would desynchronise the ranks' first timed step)
     nvc = NvlinkCounters(local) if G > 1 else None
     nv0 = nvc.read() if nvc else None
+    if nvc:
+        nvc.gpm_start()
     barrier()
     clk.start()
     time.sleep(0.3)
@@ -587,6 +631,7 @@ def gpu_arm(args, wl):
     layer.sync_weights(stream)      # the last step's (possibly deferred) replication is timed too
     end.record(stream)
     barrier()
+    gpm = nvc.gpm_stop() if nvc else None
     nv1 = nvc.read() if nvc else None
     clocks = clk.stop()
     layer.ctx.check()
@@ -709,6 +754,14 @@ def gpu_arm(args, wl):
                     "source": nvc.src}
         else:
             mine = {"error": getattr(nvc, "err", "no counters")}
+        if gpm and "error" not in gpm:  # GPM rates x the sampled interval -> bytes per step
+            scale = {"MiB/sec": 1 << 20, "MB/s": 1e6, "B/s": 1, "bytes/sec": 1}.get(gpm.get("tx_unit"), None)
+            mine["gpm"] = dict(gpm)
+            if scale and gpm.get("tx_per_sec") is not None:
+                mine["gpm"]["tx_bytes_per_step"] = gpm["tx_per_sec"] * scale * gpm["interval_s"] / K
+                mine["gpm"]["rx_bytes_per_step"] = gpm["rx_per_sec"] * scale * gpm["interval_s"] / K
+        elif gpm:
+            mine["gpm"] = gpm
         allr = [None] * G
         dist.all_gather_object(allr, mine)
         nvlink_hw = {"per_rank": allr,

@@ -39,3 +39,5 @@ int moe_plan_publish(moe_ctx *ctx, const moe_plan_t *plan_next, uint32_t epoch);
 void moe_timeline_begin(moe_ctx *ctx, void *stream);  // ctx.cu (MOE_TIMELINE development trace)
 void moe_timeline_step(moe_ctx *ctx, void *stream);
 int ctx_rank(const moe_ctx *ctx);  // ctx.cu
+int moe_update_after_dispatch(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *plan_next,
+                              const moe_adam_t *adam, void *stream, bool pdl);  // update.cu

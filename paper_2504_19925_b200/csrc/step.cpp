@@ -62,7 +62,7 @@ extern "C" int moe_step(moe_ctx *ctx, const int32_t *topk_ids, const float *gate
   if (pend) {
     st = moe_plan_publish(ctx, plan_next, pend);  // a1's result to the queued a5 stores
   } else {
-    st = moe_update(ctx, plan_cur, plan_next, adam, stream);  // a3 + a4 + a5
+    st = moe_update_after_dispatch(ctx, plan_cur, plan_next, adam, stream, ds == stream);  // a3 + a4 + a5
   }
   if (getenv("MOE_TIMELINE"))  // development trace: host phases of this step (us)
     fprintf(stderr, "HOSTSTEP rank %d: early-launch %.1f | wait C_t %.1f | plan %.1f | publish/launch %.1f\n",
