@@ -1260,7 +1260,7 @@ int moe_update_early(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_adam_t 
   *epoch = 0;
   // opt-in (MOE_EARLY_UPDATE=1): measured neutral to 2 % slower at N = 1/2/4 (the update start
   // is gated by the dispatch at N = 1 and by the de-dup pre-sum at N > 1, not by the host)
-  static const bool disabled = getenv("MOE_EARLY_UPDATE") == nullptr;
+  const bool disabled = getenv("MOE_EARLY_UPDATE") == nullptr;  // read per call (tests toggle it)
   if (disabled || !ctx || !adam || (ctx->update_kernel == 0 && !ctx->dedup) || !ctx->plan_dev ||
       !ctx->plan_pin_dev)
     return MOE_OK;

@@ -353,3 +353,16 @@ def test_zero_token_experts_step_with_zero_grads(name, G, dedup):
     tr = edge.idle_expert_trace(wl.E, wl.T, wl.k, 6, seed=11)
     run_parity(name, G, 6, trace=tr, zero_idle=True, dedup=dedup,
                rank_mode="single" if G == 1 else "virtual")
+
+
+@pytest.mark.parametrize("name,G,dedup,host_state", [("tiny-skew", 4, True, False), ("medium", 1, False, False),
+                                                     ("tiny-odd", 3, False, True), ("medium", 4, True, False)])
+def test_early_update_launch_is_bit_identical(name, G, dedup, host_state, monkeypatch):
+    """MOE_EARLY_UPDATE=1 (opt-in): moe_step queues the update before plan_{t+1} exists and the
+    kernel acquires the plan from device memory before its first a5 store --
+    every output bitwise the oracle's, including interval re-placement (KEEP steps) and the
+    host-state windows (several launches share one hand-off)."""
+    from gpu_helpers import run_parity
+    monkeypatch.setenv("MOE_EARLY_UPDATE", "1")
+    run_parity(name, G, 5, dedup=dedup, host_state=host_state, replan_interval=2,
+               rank_mode="single" if G == 1 else "virtual")

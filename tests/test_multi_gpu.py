@@ -67,3 +67,15 @@ def test_missing_peer_times_out_instead_of_hanging():
         pytest.skip("needs 2 GPUs")
     r = _torchrun(2, timeout=300, script="mp_failure.py")
     assert r.returncode == 0 and "mp_failure: OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("G,extra", [(2, ["--dedup", "--lazy", "--iters", "4"]), (4, ["--dedup", "--iters", "4", "--interval", "2"])])
+def test_early_update_launch_real_mode(G, extra, monkeypatch):
+    """The opt-in early update launch (MOE_EARLY_UPDATE=1) over NVLink: each rank's kernel
+    acquires its own host's plan_{t+1} hand-off; bit-exact vs the oracle."""
+    if torch.cuda.device_count() < G:
+        pytest.skip(f"needs {G} GPUs")
+    monkeypatch.setenv("MOE_EARLY_UPDATE", "1")
+    r = _torchrun(G, "--config", "medium", *extra)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "OK" in r.stdout
