@@ -809,7 +809,7 @@ def gpu_arm(args, wl):
     # whole step: every HBM byte of dispatch + update stage at the HBM peak, or the NVLink bytes
     t_roof_step = max((mean["stage_hbm"] + disp_hbm) / (peak_hbm * 1e9), t_nvl, t_pcie)
     # our kernels launched in the timed region, from the library's own launch counters
-    n_launch = 3 * tm["n_dispatch"] + tm["n_update_kernel"] + tm["n_presum"] + tm["n_replicate"]
+    n_launch = tm["n_dispatch_kernels"] + tm["n_update_kernel"] + tm["n_presum"] + tm["n_replicate"]
 
 
     cpu = None

@@ -56,7 +56,7 @@
 extern "C" {
 #endif
 
-#define MOE_ABI_VERSION 6
+#define MOE_ABI_VERSION 7
 #define MOE_MAX_E 256     /* experts per layer                              */
 #define MOE_MAX_G 8       /* GPUs: one NVSwitch box                         */
 #define MOE_MAX_SLOTS 4096 /* G*S                                           */
@@ -233,7 +233,9 @@ int moe_ctx_get_timing(moe_ctx *ctx, double *dispatch_ms, int64_t *n_dispatch, d
  * replicate; equals MOE_T_UPDATE without de-dup).  moe_ctx_get_timing's update_ms is
  * MOE_T_STAGE.  Host stages of moe_step (wall clock, recorded while timing is enabled):
  * MOE_T_HOST_WAIT (waiting for C_t to reach pinned host memory), MOE_T_HOST_PLAN (the
- * planner: Alg. 1 or the policy's copy) and MOE_T_HOST_LAUNCH (enqueueing the update).     */
+ * planner: Alg. 1 or the policy's copy) and MOE_T_HOST_LAUNCH (enqueueing the update);
+ * MOE_T_DISPATCH_KERNELS counts the dispatch's kernel launches (3 per call, 2 when one GPU
+ * with few tiles folds the scan into the histogram kernel).                              */
 #define MOE_T_DISPATCH 0
 #define MOE_T_UPDATE 1
 #define MOE_T_PRESUM 2
@@ -242,7 +244,8 @@ int moe_ctx_get_timing(moe_ctx *ctx, double *dispatch_ms, int64_t *n_dispatch, d
 #define MOE_T_HOST_WAIT 5
 #define MOE_T_HOST_PLAN 6
 #define MOE_T_HOST_LAUNCH 7
-#define MOE_TIMING_STAGES 8
+#define MOE_T_DISPATCH_KERNELS 8  /* n = dispatch kernel launches (2 or 3 per call), ms = 0 */
+#define MOE_TIMING_STAGES 9
 int moe_ctx_get_timing_ex(moe_ctx *ctx, double *ms, int64_t *n);
 
 /* The schedule moe_step(..., MOE_PLAN_SCHEDULED, ...) follows (moe_plan_scheduled with the

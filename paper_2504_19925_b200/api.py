@@ -169,14 +169,14 @@ class MoeContext:
     def get_timing(self) -> dict:
         """Summed CUDA-event ms and launch counts per stage since the last call: dispatch,
         update (stage), presum, replicate; plus moe_step's host wait for C_t and planner time."""
-        ms = (C.c_double * 8)()
-        n = (C.c_int64 * 8)()
+        ms = (C.c_double * 9)()
+        n = (C.c_int64 * 9)()
         check(L.lib().moe_ctx_get_timing_ex(self.handle, ms, n), "moe_ctx_get_timing_ex")
         return {"dispatch_ms": ms[0], "n_dispatch": n[0], "update_kernel_ms": ms[1],
                 "n_update_kernel": n[1], "presum_ms": ms[2], "n_presum": n[2],
                 "replicate_ms": ms[3], "n_replicate": n[3], "update_ms": ms[4], "n_update": n[4],
                 "host_wait_ms": ms[5], "n_host_wait": n[5], "host_plan_ms": ms[6], "n_host_plan": n[6],
-                "host_launch_ms": ms[7], "n_host_launch": n[7]}
+                "host_launch_ms": ms[7], "n_host_launch": n[7], "n_dispatch_kernels": n[8]}
 
     def weights_wait(self, stream=None) -> None:
         """`stream` waits until every slot weight of the last update/place is in place (only

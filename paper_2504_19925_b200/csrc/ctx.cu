@@ -510,6 +510,8 @@ extern "C" int moe_ctx_get_timing_ex(moe_ctx *ctx, double *ms_out, int64_t *n_ou
   counts[MOE_T_HOST_PLAN] = ctx->host_n[1];
   sums[MOE_T_HOST_LAUNCH] = ctx->host_ms[2];
   counts[MOE_T_HOST_LAUNCH] = ctx->host_n[2];
+  counts[MOE_T_DISPATCH_KERNELS] = ctx->disp_kernels;
+  ctx->disp_kernels = 0;
   ctx->host_ms[0] = ctx->host_ms[1] = ctx->host_ms[2] = 0.0;
   ctx->host_n[0] = ctx->host_n[1] = ctx->host_n[2] = 0;
   // without de-dup the stage is the update kernel itself

@@ -51,7 +51,65 @@ struct HistArgs {
   // (pinned counts_host + the host flag) so the planner starts before k_scan runs
   int64_t *counts_host;     // device alias of the pinned buffer, or nullptr
   uint32_t *host_flag;
+  // fused scan (G == 1 and sum_last): the last block also does k_scan's per-expert work
+  int32_t fuse_scan, S, cap;
+  ExpertInfo *einfo;
+  int32_t *slot_load, *send_count, *kept_pre;
+  int64_t *counts_dev, *drops;
+  int32_t fs[MOE_MAX_E + 1];
 };
+
+// Warp-level exclusive scan step: lane-inclusive prefix of x.
+__device__ __forceinline__ int32_t warp_incl(int32_t x, int lane) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int32_t y = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= d) x += y;
+  }
+  return x;
+}
+
+// One GPU, k_hist's last block, one warp per expert e: exactly k_scan's per-expert outputs
+// (C_e = this rank's count, base 0): replica loads q / q+1, kept = min(load, cap), send counts,
+// kept prefixes, drops, ExpertInfo, and the exclusive scan of e's tile counts in place.
+__device__ void fused_expert_scan(const HistArgs &a, int e, int32_t C, int lane) {
+  const int32_t f0 = a.fs[e], r = a.fs[e + 1] - f0;
+  const int32_t q = C / r, m = C % r;
+  const int32_t capv = a.cap > 0 ? a.cap : 0x7fffffff;
+  int32_t carry = 0, dropped = 0;
+  for (int r0 = 0; r0 < r; r0 += 32) {
+    const int rho = r0 + lane;
+    int32_t mine = 0;
+    if (rho < r) {
+      const int32_t start = rho * q + min(rho, m), load = q + (rho < m ? 1 : 0);
+      const int32_t kept = min(load, capv);
+      const int32_t lo = start, hi = min(C, start + kept);  // base 0, cnt = C
+      mine = max(0, hi - lo);
+      dropped += load - kept;
+      a.slot_load[f0 + rho] = kept;
+      a.send_count[f0 + rho] = mine;
+    }
+    const int32_t incl = warp_incl(mine, lane);
+    if (rho < r) a.kept_pre[f0 + rho] = carry + incl - mine;
+    carry += __shfl_sync(0xffffffffu, incl, 31);
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) dropped += __shfl_xor_sync(0xffffffffu, dropped, d);
+  if (lane == 0) {
+    a.counts_dev[e] = C;
+    if (a.drops) a.drops[e] = dropped;
+    a.einfo[e] = ExpertInfo{0, carry, q, m, 0xffffffffu / (uint32_t)(q + 1), q > 0 ? 0xffffffffu / (uint32_t)q : 0u};
+  }
+  int32_t *row = a.blk + (int64_t)e * a.nb_max;  // exclusive scan of the tile counts, in place
+  int32_t run = 0;
+  for (int i0 = 0; i0 < a.nb; i0 += 32) {
+    const int i = i0 + lane;
+    const int32_t c = i < a.nb ? __ldcg(row + i) : 0;
+    const int32_t incl = warp_incl(c, lane);
+    if (i < a.nb) row[i] = run + incl - c;
+    run += __shfl_sync(0xffffffffu, incl, 31);
+  }
+}
 
 __global__ void __launch_bounds__(kThreads) k_hist(const __grid_constant__ HistArgs a) {
   constexpr int kWarps = kThreads / 32;
@@ -170,6 +228,10 @@ __global__ void __launch_bounds__(kThreads) k_hist(const __grid_constant__ HistA
     if (flags)
       for (int h = 0; h < a.G; ++h) st_release_sys(&a.dst[h]->disp_flag[grank], a.epoch);
     if (host) st_release_sys(a.host_flag, a.epoch);
+  }
+  if (a.fuse_scan) {  // G == 1, few tiles: no k_scan launch (the scatter depends on this kernel);
+    const int lane = tid & 31;  // after the host release, so the planner starts first
+    for (int e = warp; e < a.E; e += kWarps) fused_expert_scan(a, e, whist[0][e], lane);
   }
 }
 
@@ -665,6 +727,20 @@ extern "C" int moe_dispatch(moe_ctx *ctx, const int32_t *topk_ids, const float *
 
   HistArgs ha{};
   ha.sum_last = (int64_t)ctx->E * nb <= 16384 ? 1 : 0;
+  // one GPU, few tiles x experts: k_hist's last block also does the scan (one launch fewer)
+  static const bool no_fuse = getenv("MOE_NO_FUSED_SCAN") != nullptr;  // A/B switch
+  ha.fuse_scan = (ctx->G == 1 && ha.sum_last && !no_fuse) ? 1 : 0;
+  if (ha.fuse_scan) {
+    ha.S = ctx->S;
+    ha.cap = out->capacity;
+    ha.einfo = ctx->einfo;
+    ha.slot_load = out->slot_load;
+    ha.send_count = out->send_count;
+    ha.kept_pre = ctx->kept_pre;
+    ha.counts_dev = out->counts_dev ? out->counts_dev : ctx->counts_dev;
+    ha.drops = out->drops;
+    for (int e = 0; e <= ctx->E; ++e) ha.fs[e] = plan->first_slot[e];
+  }
   ha.ids = topk_ids;
   ha.npairs = npairs;
   ha.k = ctx->k;
@@ -713,7 +789,8 @@ extern "C" int moe_dispatch(moe_ctx *ctx, const int32_t *topk_ids, const float *
   sa.drops = out->drops;
   sa.kept_pre = ctx->kept_pre;
   for (int e = 0; e <= ctx->E; ++e) sa.fs[e] = plan->first_slot[e];
-  MOE_CUDA_TRY(launch_pdl(k_scan, dim3(ctx->E, ctx->n_local), s, sa));
+  if (!ha.fuse_scan) MOE_CUDA_TRY(launch_pdl(k_scan, dim3(ctx->E, ctx->n_local), s, sa));
+  if (ctx->timing) ctx->disp_kernels += (ha.fuse_scan ? 1 : 2) + (npairs > 0 ? 1 : 0);
   ctx->counts_pending = true;
 
   ScatterArgs ca{};

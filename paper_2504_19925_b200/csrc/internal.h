@@ -148,6 +148,7 @@ struct moe_ctx {
   // measurement hooks (moe_ctx_set_timing): event pairs per stage, recycled
   bool timing;
   double host_ms[3];    // MOE_T_HOST_WAIT, _PLAN, _LAUNCH (moe_step, wall clock)
+  int64_t disp_kernels; // MOE_T_DISPATCH_KERNELS (while timing is enabled)
   int64_t host_n[3];
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool, ev_disp, ev_upd, ev_presum, ev_repl, ev_stage;
 };

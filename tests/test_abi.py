@@ -37,7 +37,7 @@ def test_exports_every_declared_symbol(lib):
     assert declared == set(_lib.EXPORTED)
     for name in declared:
         assert hasattr(lib, name), name
-    assert lib.moe_abi_version() == 6
+    assert lib.moe_abi_version() == 7
     from paper_2504_19925_b200 import _build
     assert lib.moe_build_id().decode() == _build.source_hash() == _build.built_id()
     assert lib.moe_status_str(3) == b"MOE_ERR_DATA"
