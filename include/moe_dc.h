@@ -221,14 +221,14 @@ int moe_ctx_export(moe_ctx *ctx, void *out);
 int moe_ctx_connect(moe_ctx *ctx, const void *all);
 
 /* Measurement hooks.  While enabled, the library records CUDA events on the launching stream
- * around each dispatch (its three kernels) and around each update kernel launch (excluding
+ * around each dispatch (its two or three kernels) and around each update kernel launch (excluding
  * the cross-GPU barriers).  moe_ctx_get_timing synchronises on the recorded events, returns
  * the summed milliseconds and launch counts since the previous call, and clears them.      */
 int moe_ctx_set_timing(moe_ctx *ctx, int32_t enable);
 int moe_ctx_get_timing(moe_ctx *ctx, double *dispatch_ms, int64_t *n_dispatch, double *update_ms,
                        int64_t *n_update);
 /* Finer breakdown (also cleared by either getter): ms[MOE_TIMING_STAGES] / n[...] for
- * MOE_T_DISPATCH (3 kernels), MOE_T_UPDATE (the update kernel alone), MOE_T_PRESUM and
+ * MOE_T_DISPATCH (its kernels), MOE_T_UPDATE (the update kernel alone), MOE_T_PRESUM and
  * MOE_T_REPLICATE (de-dup kernels), MOE_T_STAGE (the whole update stage: presum + update +
  * replicate; equals MOE_T_UPDATE without de-dup).  moe_ctx_get_timing's update_ms is
  * MOE_T_STAGE.  Host stages of moe_step (wall clock, recorded while timing is enabled):
@@ -355,7 +355,7 @@ int moe_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *plan_
  *   moe_update(plan_cur, plan_next, adam)                    a3+a4+a5  (device, async)
  * plan_next: caller-allocated arrays, filled here.  Returns after the update is enqueued.
  * Scheduling inside: with MOE_OPT_DEDUP the local partial sums start first on a library side
- * stream; the three dispatch kernels run on a highest-priority library stream; both are
+ * stream; the dispatch kernels run on a highest-priority library stream; both are
  * joined to `stream` by events, so the caller sees ordinary stream semantics.
  * policy: a moe_plan_policy -- MOE_PLAN_SCHEDULED follows the context's schedule
  * (moe_ctx_set_schedule; the library decides re-place vs keep from adam->step), MOE_PLAN_KEEP

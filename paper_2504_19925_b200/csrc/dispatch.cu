@@ -6,7 +6,8 @@
 // are ranked within their expert in global order (rank, token, choice); the first
 // m = C_e mod r_e replicas take q+1 = C_e div r_e + 1 pairs, the rest q, in contiguous chunks.
 //
-// Three launches per call, all integer work, bit-exact and deterministic (no atomics
+// Three launches per call (two on one GPU when E x tiles <= 16 K: k_hist's last block then
+// does k_scan's work, fused_expert_scan), all integer work, bit-exact and deterministic (no atomics
 // decide any order):
 //   K1 k_hist    per-tile expert histograms (warp-aggregated shared-memory atomics); the
 //                last tile of each rank publishes the rank's [E] counts into every GPU's
@@ -37,6 +38,7 @@ __device__ __forceinline__ uint32_t atom_add_acq_rel_gpu(uint32_t *p, uint32_t v
 
 struct HistArgs {
   int32_t sum_last;  // E * nb small: the last block sums the tile counts instead of atomics
+  int32_t no_total;  // one GPU, E * nb large: no per-rank totals here (k_scan sums the rows)
   const int32_t *ids;
   int64_t npairs;  // pairs per rank = T*k
   int32_t k, E, G, rank, real, nb, nb_max, tile;
@@ -184,8 +186,9 @@ __global__ void __launch_bounds__(kThreads) k_hist(const __grid_constant__ HistA
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) h += whist[w][e];
     blk[(int64_t)e * a.nb_max + b] = h;
-    if (h && !a.sum_last) atomicAdd(a.cnt_local + v * a.E + e, h);
+    if (h && !a.sum_last && !a.no_total) atomicAdd(a.cnt_local + v * a.E + e, h);
   }
+  if (a.no_total) return;  // one GPU, many tiles: k_scan sums the rows and publishes C_e
   // ticket: bar.sync orders the block's writes before thread 0's acq_rel atomic (release is
   // cumulative); the last block's acquire makes every block's counts visible to it
   __syncthreads();
@@ -236,6 +239,7 @@ __global__ void __launch_bounds__(kThreads) k_hist(const __grid_constant__ HistA
 }
 
 struct ScanArgs {
+  int32_t rowsum;  // one GPU, many tiles: C_e from the scanned row (k_hist counted nothing)
   int32_t E, G, S, rank, real, nb, nb_max;
   uint32_t epoch;
   int32_t parity;
@@ -306,7 +310,18 @@ __global__ void __launch_bounds__(kThreads) k_scan(const __grid_constant__ ScanA
   // bit and writes nothing either -- but still take (and reset) the block ticket below, so the
   // next dispatch finds the counter at zero.  The context stays poisoned until moe_ctx_check.
   if (ok) {
-  if (warp == 0) {  // warp-parallel: C_e and this rank's base over GPUs
+  if (a.rowsum) {  // one GPU, many tiles: k_hist skipped its count atomics; C_e = the row total
+    const int32_t *rowp = a.blk + ((int64_t)v * a.E + e) * a.nb_max;
+    int32_t part = 0;
+    for (int i = tid; i < a.nb; i += kThreads) part += __ldcg(rowp + i);
+    int32_t tot;
+    block_exclusive_scan(part, wsum, &tot);
+    if (tid == 0) {
+      s_base = 0;
+      s_cnt = tot;
+      s_C = tot;
+    }
+  } else if (warp == 0) {  // warp-parallel: C_e and this rank's base over GPUs
     const int32_t(*x)[MOE_MAX_E] = a.sync->xcnt[a.parity];
     const int32_t c = lane < a.G ? ld_cg(&x[lane][e]) : 0;
     int32_t C = c, base = lane < grank ? c : 0;
@@ -392,8 +407,8 @@ __global__ void __launch_bounds__(kThreads) k_scan(const __grid_constant__ ScanA
   if (tid == 0) s_last = atom_add_acq_rel_gpu(a.scan_done, 1u) == gridDim.x * gridDim.y - 1;
   __syncthreads();
   if (s_last) {
-    const bool publish = (a.G > 1 || !a.counts_host) &&   // on one GPU k_hist already did
-                         !(__ldcg(a.err) & kErrTimeout);   // never release incomplete counts
+    const bool publish = (a.G > 1 || a.rowsum || !a.counts_host) &&  // (one GPU: k_hist did,
+                         !(__ldcg(a.err) & kErrTimeout);   // unless rowsum) never incomplete counts
     if (publish && a.counts_host)
       for (int x = tid; x < a.E; x += kThreads) a.counts_host[x] = __ldcg(a.counts_dev + x);
     __syncthreads();
@@ -730,6 +745,9 @@ extern "C" int moe_dispatch(moe_ctx *ctx, const int32_t *topk_ids, const float *
   // one GPU, few tiles x experts: k_hist's last block also does the scan (one launch fewer)
   static const bool no_fuse = getenv("MOE_NO_FUSED_SCAN") != nullptr;  // A/B switch
   ha.fuse_scan = (ctx->G == 1 && ha.sum_last && !no_fuse) ? 1 : 0;
+  // one GPU, many tiles: skip k_hist's 2 x E x tiles count atomics and its ticket (all tiles
+  // hitting the same counters at once); k_scan takes C_e from the row it scans anyway
+  ha.no_total = (ctx->G == 1 && !ha.sum_last && !no_fuse) ? 1 : 0;
   if (ha.fuse_scan) {
     ha.S = ctx->S;
     ha.cap = out->capacity;
@@ -766,6 +784,7 @@ extern "C" int moe_dispatch(moe_ctx *ctx, const int32_t *topk_ids, const float *
   MOE_CUDA_TRY(cudaGetLastError());
 
   ScanArgs sa{};
+  sa.rowsum = ha.no_total;
   sa.E = ctx->E;
   sa.G = ctx->G;
   sa.S = ctx->S;

@@ -366,3 +366,16 @@ def test_early_update_launch_is_bit_identical(name, G, dedup, host_state, monkey
     monkeypatch.setenv("MOE_EARLY_UPDATE", "1")
     run_parity(name, G, 5, dedup=dedup, host_state=host_state, replan_interval=2,
                rank_mode="single" if G == 1 else "virtual")
+
+
+@pytest.mark.parametrize("E,k,T,cf", [(200, 4, 16384, 0.0), (256, 8, 8192, 1.0), (20, 2, 1 << 18, 0.0)])
+def test_one_gpu_dispatch_modes(E, k, T, cf):
+    """One GPU: with E x tiles > 16 K the histogram kernel skips its count atomics and k_scan
+    takes C_e from the tile rows it scans (and publishes it); with E x tiles <= 16 K k_hist's last
+    block does the whole scan (fused_expert_scan).  Both against the oracle, every output."""
+    from gpu_helpers import run_parity
+    from oracle.dispatch import slot_capacity
+    wl = configs.Workload(f"modes{E}", E=E, d=64, ffn=1, mats=1, k=k, T=T, slots_total=max(E, 256),
+                          trace="walk-spike", G_default=1)
+    cap = slot_capacity(cf, T, k, wl.slots_total) if cf > 0 else 0
+    run_parity(wl, 1, 3, seed=321 + E, capacity=cap, rank_mode="single")
