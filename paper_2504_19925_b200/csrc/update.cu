@@ -1275,8 +1275,11 @@ int moe_update_early(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_adam_t 
   // launched between the scatter and the update)
   st = launch_update(ctx, plan_cur, nullptr, adam, 0, stream, ep, pdl && !ctx->host_state && !ctx->dedup &&
                                                                        !ctx->timing && !ctx->tl_on);
-  if (st) return st;
   ctx->plan_epoch = ep;
+  if (st) {  // a kernel of this launch may already be queued: release it (it places nothing)
+    moe_plan_publish(ctx, nullptr, ep);
+    return st;
+  }
   *epoch = ep;
   return MOE_OK;
 }
