@@ -218,7 +218,7 @@ extern "C" int moe_ctx_create(const moe_ctx_desc *d, moe_ctx **out) {
   chk(cudaMalloc(&c->kept_pre, sizeof(int32_t) * n_local * c->G * c->S));
   chk(cudaMalloc(&c->counts_dev, sizeof(int64_t) * c->E));
   chk(cudaMalloc(&c->err, sizeof(int32_t)));
-  chk(cudaMalloc(&c->item_ctr, 3 * sizeof(unsigned long long)));
+  chk(cudaMalloc(&c->item_ctr, (3 + 3 + MOE_MAX_G) * sizeof(unsigned long long)));  // + fused pre-sum
   chk(cudaMalloc(&c->scan_done, sizeof(uint32_t)));
   chk(cudaMalloc(&c->plan_dev, sizeof(PlanDev)));
   chk(cudaHostAlloc(&c->plan_pin, sizeof(PlanDev), cudaHostAllocMapped));
@@ -245,7 +245,7 @@ extern "C" int moe_ctx_create(const moe_ctx_desc *d, moe_ctx **out) {
     chk(cudaMemset(c->cnt_local, 0, sizeof(int32_t) * n_local * c->E));
     chk(cudaMemset(c->done, 0, sizeof(uint32_t) * n_local));
     chk(cudaMemset(c->err, 0, sizeof(int32_t)));
-    chk(cudaMemset(c->item_ctr, 0, 3 * sizeof(unsigned long long)));
+    chk(cudaMemset(c->item_ctr, 0, (3 + 3 + MOE_MAX_G) * sizeof(unsigned long long)));
     chk(cudaMemset(c->scan_done, 0, sizeof(uint32_t)));
     chk(cudaMemset(c->plan_dev, 0, sizeof(PlanDev)));
     memset(c->plan_pin, 0, sizeof(PlanDev));

@@ -31,6 +31,7 @@ struct SyncBuf {
   alignas(128) uint32_t disp_flag[MOE_MAX_G];   // count exchange arrived (epoch)
   alignas(128) uint32_t upd_in[MOE_MAX_G];      // update barrier-in (epoch)
   alignas(128) uint32_t upd_out[MOE_MAX_G];     // update barrier-out (epoch)
+  alignas(128) uint32_t pre_ready[MOE_MAX_G];   // de-dup partials of GPU g complete (epoch)
   alignas(128) int32_t xcnt[2][MOE_MAX_G][MOE_MAX_E];  // per-rank expert counts, by epoch parity
 };
 

@@ -72,6 +72,22 @@ struct UpdArgs {
   const int32_t *fsn_host;
   const uint8_t *hfn_host;
   const uint32_t *pflag_host;
+  // De-dup pre-sum fused into this kernel (moe_step / moe_update with MOE_OPT_DEDUP): the
+  // consumer warps of CTAs blockIdx < pre_ctas first drain the pre-sum items (partial row q of
+  // local rank v, chunk c over [0, P)); the CTA completing GPU h's last item releases
+  // pre_ready[h] = epoch on every GPU, and producers acquire pre_ready[h] once before their first
+  // partial pull from h.  The update therefore starts without waiting for the pre-sum.
+  int32_t pre_fused, pre_ctas;
+  int64_t pre_nchunks;                    // kChunk chunks over [0, P)
+  int32_t pre_qoff[MOE_MAX_G + 1];        // prefix of partial rows over local ranks
+  int16_t pre_qe[MOE_MAX_G][MOE_MAX_E];   // expert of partial row q of local rank v
+  const uint16_t *grads_local[MOE_MAX_G]; // local rank v: bf16 [S][P]
+  float *presum_local[MOE_MAX_G];         // local rank v: fp32 [nq_max][P]
+  unsigned long long *pre_ctr;            // [0] claims [1] failed claims [2 + v] items done
+  // item order with a single owner: experts needing no remote partial first (elist[0, n_phaseA)),
+  // so CTAs work while the other GPUs' pre-sums finish; -1 = plain chunk-major
+  int32_t n_phaseA;
+  uint8_t elist[MOE_MAX_E];
   // development trace (env MOE_KTRACE): globaltimer stamps folded with atomics, printed by the
   // CTA that completes barrier-out.  [0] min start [1] max start [2] max barrier-in done
   // [3] min consumer done [4] max consumer done
@@ -406,6 +422,87 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       : "memory");
 }
 
+// One fused pre-sum item by the 256 consumer threads of a CTA (the k_presum computation):
+// partial row q of local rank v (its expert e's replicas on GPU h = o_begin + v, ascending slot
+// order, fp32 from bf16, reading A11's per-GPU term) over chunk c of [0, P), skipping chunks
+// inside GPU h's own owner range (its owner reads the slices).  Returns the local rank v.
+__device__ __forceinline__ int presum_item(const UpdArgs &a, int64_t it, int tid) {
+  const int row = (int)(it / a.pre_nchunks);
+  const int64_t c = it - (int64_t)row * a.pre_nchunks;
+  int v = 0;
+  while (row >= a.pre_qoff[v + 1]) ++v;
+  const int q = row - a.pre_qoff[v];
+  const int e = a.pre_qe[v][q];
+  const int h = a.o_begin + v;
+  if (c * kChunk >= (int64_t)h * a.Pg && (c + 1) * kChunk <= (int64_t)(h + 1) * a.Pg) return v;
+  const int64_t i = c * kChunk + (int64_t)tid * kVec;
+  if (i >= a.P) return v;
+  const int ja = max(a.fs_cur[e], h * a.S), jb = min(a.fs_cur[e + 1], (h + 1) * a.S);
+  const uint16_t *base = a.grads_local[v] + i;
+  float part[8];
+  for (int j = ja; j < jb; j += kBatch) {  // ascending slot order, loads batched
+    const int n = min(kBatch, jb - j);
+    uint4 buf[kBatch];
+#pragma unroll
+    for (int b = 0; b < kBatch; ++b)
+      if (b < n) buf[b] = ld_stream(base + (int64_t)(j + b - h * a.S) * a.P);
+#pragma unroll
+    for (int b = 0; b < kBatch; ++b)
+      if (b < n) {
+        float g8[8];
+        unpack_bf16x8(buf[b], g8);
+        if (j + b == ja) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) part[k] = g8[k];
+        } else {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) part[k] = __fadd_rn(part[k], g8[k]);
+        }
+      }
+  }
+  float4 *dst = reinterpret_cast<float4 *>(a.presum_local[v] + (int64_t)q * a.P + i);
+  dst[0] = make_float4(part[0], part[1], part[2], part[3]);
+  dst[1] = make_float4(part[4], part[5], part[6], part[7]);
+  return v;
+}
+
+// Consumers of a pre-sum CTA: claim and process pre-sum items until none are left; the CTA that
+// completes a GPU's last item releases its pre_ready flag everywhere.
+__device__ void presum_phase(const UpdArgs &a, int tid) {
+  __shared__ int64_t s_pit[2];
+  const int64_t total = (int64_t)a.pre_qoff[a.o_count] * a.pre_nchunks;
+  for (int k = 0;; ++k) {
+    if (tid == 0) s_pit[k & 1] = (int64_t)atomicAdd(a.pre_ctr, 1ull);
+    asm volatile("bar.sync 2, %0;" ::"r"(kThreads) : "memory");
+    const int64_t pit = s_pit[k & 1];
+    if (pit >= total) {
+      // every pre-sum CTA fails exactly one claim: the last one resets the claim counters
+      if (tid == 0 && atomicAdd(a.pre_ctr + 1, 1ull) == (unsigned long long)a.pre_ctas - 1) {
+        a.pre_ctr[0] = 0;
+        a.pre_ctr[1] = 0;
+        __threadfence();
+      }
+      return;
+    }
+    const int v = presum_item(a, pit, tid);
+    // the CTA's partial stores, then one acq_rel completion count (release cumulative over the
+    // bar.sync); the CTA counting GPU v's last item acquires every other CTA's items and
+    // releases them to the peers at system scope
+    asm volatile("bar.sync 2, %0;" ::"r"(kThreads) : "memory");
+    if (tid == 0) {
+      const unsigned long long need = (unsigned long long)(a.pre_qoff[v + 1] - a.pre_qoff[v]) * a.pre_nchunks;
+      unsigned long long done;
+      asm volatile("atom.add.acq_rel.gpu.global.u64 %0, [%1], 1;" : "=l"(done) : "l"(a.pre_ctr + 2 + v) : "memory");
+      if (done == need - 1) {  // GPU v's partials are complete
+        a.pre_ctr[2 + v] = 0;
+        __threadfence_system();
+        const int h = a.o_begin + v;
+        for (int g = 0; g < a.G; ++g) st_release_sys(&a.sync_peer[g]->pre_ready[h], a.epoch);
+      }
+    }
+  }
+}
+
 template <int kGradSlots>
 __global__ void __launch_bounds__(kTmaThreads, 2) k_update_tma(const __grid_constant__ UpdArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -457,6 +554,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_update_tma(const __grid_cons
       for (int h = 0; h < a.G; ++h) wait_flag(&a.sync_local->upd_in[h], a.epoch, a.err);
     if (a.ktrace) atomicMax(a.ktrace + 2, globaltimer());
     uint32_t si = 0, gi_ = 0;
+    uint32_t pre_ok = 0;  // GPUs whose fused pre-sum this producer has acquired
     for (;;) {
       // dynamic scheduling: claim the next item (chunk-major order, see kItemOrder note)
       const int64_t it = (int64_t)atomicAdd(a.item_ctr, 1ull);
@@ -474,11 +572,26 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_update_tma(const __grid_cons
         }
         break;
       }
-      slot_item[s] = it;
-      const int o = a.o_begin + (int)(it / per_owner);
-      const int64_t rem = it - (int64_t)(o - a.o_begin) * per_owner;
-      const int e = (int)(rem % a.E);
-      const int64_t c = a.c_lo + rem / a.E;
+      int o, e;
+      int64_t c;
+      if (a.n_phaseA >= 0) {  // single owner: phase A (no remote partial) experts first
+        o = a.o_begin;
+        const int64_t nA = a.n_phaseA, spanA = nA * a.c_cnt;
+        if (it < spanA) {
+          c = a.c_lo + it / nA;
+          e = a.elist[it % nA];
+        } else {
+          const int64_t nB = a.E - nA, r2 = it - spanA;
+          c = a.c_lo + r2 / nB;
+          e = a.elist[nA + r2 % nB];
+        }
+      } else {
+        o = a.o_begin + (int)(it / per_owner);
+        const int64_t rem = it - (int64_t)(o - a.o_begin) * per_owner;
+        e = (int)(rem % a.E);
+        c = a.c_lo + rem / a.E;
+      }
+      slot_item[s] = ((int64_t)o << 40) | (c << 8) | e;  // the consumers decode the packed item
       const int64_t loc0 = c * kChunk;
       const uint32_t nval = (uint32_t)(a.Pg - loc0 < kChunk ? a.Pg - loc0 : kChunk);
       const int64_t so = (int64_t)e * a.spitch + loc0 - a.s_off;
@@ -496,6 +609,11 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_update_tma(const __grid_cons
         const int jb = min(j1, (h + 1) * a.S);
         const int q = (a.dedup && h != o) ? a.pq[e][h] : -1;  // own GPU: read the slices
         if (q >= 0) {  // de-dup: GPU h's fp32 partial of this run, as two 4 KB ring slots
+          if (a.pre_fused && !(pre_ok & (1u << h))) {  // h's fused pre-sum done (once per GPU)
+            wait_flag(&a.sync_local->pre_ready[h], a.epoch, a.err);
+            asm volatile("fence.proxy.async;" ::: "memory");  // before the bulk (async-proxy) reads
+            pre_ok |= 1u << h;
+          }
           const float *src = a.presum[h] + (int64_t)q * P + g0;
           const uint32_t nA = nval < kChunk / 2 ? nval : kChunk / 2, nB = nval - nA;
           for (int half = 0; half < 2; ++half) {
@@ -532,15 +650,15 @@ __global__ void __launch_bounds__(kTmaThreads, 2) k_update_tma(const __grid_cons
   const int tid = threadIdx.x;
   uint32_t si = 0, gi_ = 0;
   int plan_state = 0;  // early launch: 0 not yet seen, 1 plan_{t+1} available, 2 timed out
+  if (a.pre_fused && (int)blockIdx.x < a.pre_ctas) presum_phase(a, tid);  // then the update items
   for (;;) {
     const int s = si % kStateSlots;
     mbar_wait(st_full + s, (si / kStateSlots) & 1);
     const int64_t it = slot_item[s];
     if (it < 0) break;
-    const int o = a.o_begin + (int)(it / per_owner);
-    const int64_t rem = it - (int64_t)(o - a.o_begin) * per_owner;
-    const int e = (int)(rem % a.E);
-    const int64_t c = a.c_lo + rem / a.E;
+    const int o = (int)(it >> 40);
+    const int e = (int)(it & 0xff);
+    const int64_t c = (it >> 8) & 0xffffffffll;
     const int64_t loc = c * kChunk + (int64_t)tid * 4;  // group A; group B at loc + H
     // early launch, plan already acquired: fetch this item's run of plan_{t+1} now, so the
     // loads overlap the reduce instead of preceding the stores
@@ -883,6 +1001,14 @@ int build_presum(moe_ctx *ctx, const moe_plan_t *plan_cur, int8_t (&pq)[MOE_MAX_
   return MOE_OK;
 }
 
+// De-dup pre-sum inside the update kernel (default; MOE_PRESUM_SEPARATE=1: a separate
+// k_presum before it, the round-1 design) -- not with host-resident state (windowed launches)
+// nor with the register-staged update kernel.
+bool presum_fused(const moe_ctx *ctx) {
+  static const bool separate = getenv("MOE_PRESUM_SEPARATE") != nullptr;
+  return ctx->dedup && !ctx->host_state && !separate;
+}
+
 // Shared launcher of moe_update (place_only = 0) and moe_place (place_only = 1).
 // pend_epoch != 0 (moe_step's early launch): plan_next is NULL -- the kernels read plan_{t+1}
 // from ctx->plan_dev once its epoch word reaches pend_epoch (moe_plan_publish).
@@ -899,6 +1025,7 @@ int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *pl
   }
 
   UpdArgs a{};
+  a.n_phaseA = -1;  // plain chunk-major item order unless the fused pre-sum reorders it
   a.E = ctx->E;
   a.G = ctx->G;
   a.S = ctx->S;
@@ -982,6 +1109,32 @@ int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *pl
     for (int e = 0; pre && e <= ctx->E; ++e) pre = ctx->presum_fs[e] == plan_cur->first_slot[e];
     if (pre) {
       MOE_CUDA_TRY(cudaStreamWaitEvent(s, ctx->ev_presum_done, 0));
+    } else if (pa.nq_total > 0 && presum_fused(ctx)) {  // the update kernel does the pre-sum
+      a.pre_fused = 1;
+      a.pre_nchunks = pa.nchunks;
+      for (int v = 0; v <= ctx->n_local; ++v) a.pre_qoff[v] = pa.qoff[v];
+      memcpy(a.pre_qe, pa.q_e, sizeof(a.pre_qe));
+      for (int v = 0; v < ctx->n_local; ++v) {
+        a.grads_local[v] = pa.grads[v];
+        a.presum_local[v] = pa.presum[v];
+      }
+      a.pre_ctr = ctx->item_ctr + 3;
+      if (ctx->n_local == 1) {  // one owner: experts that need no other GPU's partial first
+        const int o = a.o_begin;
+        int nA = 0;
+        for (int e = 0; e < ctx->E; ++e) {
+          bool remote = false;
+          for (int h = 0; h < ctx->G; ++h) remote |= (h != o && a.pq[e][h] >= 0);
+          if (!remote) a.elist[nA++] = (uint8_t)e;
+        }
+        int nB = nA;
+        for (int e = 0; e < ctx->E; ++e) {
+          bool remote = false;
+          for (int h = 0; h < ctx->G; ++h) remote |= (h != o && a.pq[e][h] >= 0);
+          if (remote) a.elist[nB++] = (uint8_t)e;
+        }
+        a.n_phaseA = nA;
+      }
     } else if (pa.nq_total > 0) {
       const int64_t grid = std::min<int64_t>((int64_t)pa.nq_total * pa.nchunks, (int64_t)ctx->num_sms * 8);
       const auto pev = timing_begin(ctx, s);
@@ -1035,6 +1188,10 @@ int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *pl
       }
     } else {
       const int64_t grid = std::min<int64_t>(items, (int64_t)ctx->num_sms * 2);
+      if (ka.pre_fused) {  // CTAs that drain the pre-sum first (default: one per SM)
+        static const int want = getenv("MOE_PRESUM_CTAS") ? atoi(getenv("MOE_PRESUM_CTAS")) : 0;
+        ka.pre_ctas = (int)std::max<int64_t>(1, std::min<int64_t>(grid, want > 0 ? want : ctx->num_sms));
+      }
       if (grid > 0) {
         const auto tev = timing_begin(ctx, s);
         if (pdl_after_dispatch && !ka.ktrace && !tev.first) {
@@ -1196,6 +1353,7 @@ extern "C" int moe_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_pl
 // highest-priority stream.  moe_update then waits on its event instead of launching it.
 int moe_presum_prelaunch(moe_ctx *ctx, const moe_plan_t *plan_cur, void *stream) {
   ctx->presum_ready = false;
+  if (presum_fused(ctx)) return MOE_OK;  // the update kernel does it
   static const bool serial = getenv("MOE_PRESUM_SERIAL") != nullptr;  // A/B: pre-sum after the dispatch
   if (!ctx->dedup || serial) return MOE_OK;
   int st = moe_validate_plan(ctx, plan_cur, "moe_step(plan_cur)");
