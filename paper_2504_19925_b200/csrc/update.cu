@@ -72,7 +72,7 @@ struct UpdArgs {
   const int32_t *fsn_host;
   const uint8_t *hfn_host;
   const uint32_t *pflag_host;
-  // De-dup pre-sum fused into this kernel (moe_step / moe_update with MOE_OPT_DEDUP): the
+  // De-dup pre-sum fused into this kernel (opt-in MOE_PRESUM_FUSED, see presum_fused()): the
   // consumer warps of CTAs blockIdx < pre_ctas first drain the pre-sum items (partial row q of
   // local rank v, chunk c over [0, P)); the CTA completing GPU h's last item releases
   // pre_ready[h] = epoch on every GPU, and producers acquire pre_ready[h] once before their first
@@ -1001,12 +1001,15 @@ int build_presum(moe_ctx *ctx, const moe_plan_t *plan_cur, int8_t (&pq)[MOE_MAX_
   return MOE_OK;
 }
 
-// De-dup pre-sum inside the update kernel (default; MOE_PRESUM_SEPARATE=1: a separate
-// k_presum before it, the round-1 design) -- not with host-resident state (windowed launches)
-// nor with the register-staged update kernel.
+// De-dup pre-sum inside the update kernel: opt-in (MOE_PRESUM_FUSED=1, read per call so tests
+// can toggle it) -- bit-identical, but measured slower than the separate k_presum concurrent
+// with the dispatch at every point on a 4xB200 box (profiles/r02/presum_ab_*.json: Qwen3 N = 4
+// 1.183 vs 1.089 ms, N = 2 1.960 vs 1.774, GPT-small N = 4 0.455 vs 0.393, stress N = 4 1.195
+// vs 1.161): the pre-sum CTAs' SMs start their update items late and the slowest GPU's partials
+// gate the owners' pulls.  Not with host-resident state (windowed launches).  De-dup always runs
+// the TMA kernel, which is the one that carries the fused phase.
 bool presum_fused(const moe_ctx *ctx) {
-  static const bool separate = getenv("MOE_PRESUM_SEPARATE") != nullptr;
-  return ctx->dedup && !ctx->host_state && !separate;
+  return ctx->dedup && !ctx->host_state && getenv("MOE_PRESUM_FUSED") != nullptr;
 }
 
 // Shared launcher of moe_update (place_only = 0) and moe_place (place_only = 1).

@@ -96,6 +96,20 @@ def test_dedup_is_bit_identical(name, G, iters, sampled):
         run_parity(name, G, iters, dedup=True, lazy_replicate=True)
 
 
+@pytest.mark.parametrize("name,G,iters,sampled", [("tiny-skew", 4, 12, False), ("medium", 4, 4, False),
+                                                  ("medium", 2, 4, False), ("gpt-small", 8, 2, True)])
+def test_fused_presum_is_bit_identical(name, G, iters, sampled, monkeypatch):
+    """The opt-in de-dup pre-sum inside the update kernel (MOE_PRESUM_FUSED=1: consumer warps of
+    the first CTAs compute the partials, owners acquire per-GPU pre_ready flags before pulling
+    them) gives exactly the oracle's bits, also with lazy replication and interval re-placement."""
+    from gpu_helpers import run_parity
+    monkeypatch.setenv("MOE_PRESUM_FUSED", "1")
+    wl = configs.CONFIGS[name]
+    run_parity(name, G, iters, dedup=True, idx=_sample_idx(wl.P, G) if sampled else None)
+    if not sampled:
+        run_parity(name, G, iters, dedup=True, lazy_replicate=True, replan_interval=2)
+
+
 @pytest.mark.parametrize("name,G,cf", [("tiny-skew", 4, 1.0), ("tiny-odd", 3, 0.5), ("medium", 4, 1.25),
                                        ("medium", 1, 1.0)])
 def test_capacity_and_drops(name, G, cf):

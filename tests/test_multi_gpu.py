@@ -79,3 +79,16 @@ def test_early_update_launch_real_mode(G, extra, monkeypatch):
     r = _torchrun(G, "--config", "medium", *extra)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "OK" in r.stdout
+
+
+@pytest.mark.parametrize("G,extra", [(2, ["--dedup", "--lazy", "--iters", "4"]),
+                                     (4, ["--dedup", "--iters", "4", "--cf", "1.25"])])
+def test_fused_presum_real_mode(G, extra, monkeypatch):
+    """The opt-in fused pre-sum (MOE_PRESUM_FUSED=1) over NVLink: partials released per GPU with
+    system-scope flags, acquired by every owner before its first bulk pull; bit-exact."""
+    if torch.cuda.device_count() < G:
+        pytest.skip(f"needs {G} GPUs")
+    monkeypatch.setenv("MOE_PRESUM_FUSED", "1")
+    r = _torchrun(G, "--config", "medium", *extra)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "OK" in r.stdout
