@@ -145,14 +145,6 @@ __device__ __forceinline__ void tok_dest(const TokArgs &a, int64_t pbase, int la
 // A warp per token (grid stride): it reads the token's row ONCE, 32 x kTokU vectors at a time
 // (the next token's first chunk is prefetched before the current stores), and stores each
 // chunk to the k destination rows (pointers shuffled from lanes j < k; k > 32: per-pair loads).
-// kCS: streaming stores (st.global.cs, evict-first) for the k destination rows, which nothing
-// reads before the expert FFN -- an A/B variant (MOE_TOK_STORE_CS=1).
-__device__ __forceinline__ void st_cs(uint4 *p, uint4 v) {
-  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
-               : "memory");
-}
-
-template <bool kCS>
 __global__ void __launch_bounds__(kThreads, 4) k_tok_dispatch(TokArgs a) {
   arrive_and_wait(a);
   const int lane = threadIdx.x & 31;
@@ -209,11 +201,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_tok_dispatch(TokArgs a) {
 #pragma unroll
         for (int u = 0; u < kTokU; ++u) {
           const int64_t c = c0 + u * 32 + lane;
-          if (c < a.dv) {
-            const uint4 val = a.gate ? scale8(x[u], g) : x[u];
-            if (kCS) st_cs(dst + c, val);
-            else dst[c] = val;
-          }
+          if (c < a.dv) dst[c] = a.gate ? scale8(x[u], g) : x[u];
         }
       }
 #pragma unroll
@@ -586,8 +574,7 @@ extern "C" int moe_token_dispatch(moe_tokx *x, const void *const *src, int64_t T
   cudaStream_t s = (cudaStream_t)stream;
   const bool sync = c->rank >= 0 && c->G > 1;
   a.epoch = sync ? ++x->arrive_epoch : 0;
-  if (getenv("MOE_TOK_STORE_CS")) MOE_CUDA_TRY(launch_tok(k_tok_dispatch<true>, x->blocks, s, a));
-  else MOE_CUDA_TRY(launch_tok(k_tok_dispatch<false>, x->blocks, s, a));
+  MOE_CUDA_TRY(launch_tok(k_tok_dispatch, x->blocks, s, a));
   if (sync) {
     // the done flags reuse the arrive epoch (one dispatch per arrive increment is enough:
     // done[] is written only by dispatches, and epochs only grow)
