@@ -260,7 +260,8 @@ int moe_ctx_check(moe_ctx *ctx, void *stream);
 /* Blocks the calling host thread until the C_e of the most recent moe_dispatch have landed
  * in out->counts_host: a dispatch kernel writes them to the pinned buffer and releases a
  * pinned host flag (system scope) that this call spins on -- the histogram kernel's last
- * block when G == 1, the scan kernel's last block when G > 1 -- BEFORE the scatter kernel,
+ * block when G == 1 and E x tiles <= 16 K (it also does the scan then), the scan kernel's last
+ * block otherwise (G > 1, or one GPU with many tiles) -- BEFORE the scatter kernel,
  * so the host planner (step 6 may "execute earlier, even right after step 1", PAPER.md:709
  * fn) overlaps the rest of the dispatch.  ONLY counts_host is guaranteed on return: every
  * other output of the dispatch (counts_dev, slot_load, send_count, drops, the per-pair
@@ -344,8 +345,8 @@ int moe_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *plan_
  * One whole iteration, natively, in the paper's order (fig:design_diagram):
  *   moe_dispatch(plan_cur)                                   a0 + a2   (device, async)
  *   wait for C_t in out->counts_host (pinned; required)     (host spins on a pinned flag that
- *                                                             the histogram (G == 1) or scan
- *                                                             (G > 1) kernel releases; the
+ *                                                             the histogram (G == 1, few
+ *                                                             tiles) or scan kernel releases; the
  *                                                             rest of the dispatch keeps
  *                                                             running -- only counts_host is
  *                                                             complete at that point)
