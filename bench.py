@@ -252,7 +252,8 @@ def update_stage_bytes(fs_cur, fs_next, G: int, S: int, P: int, E: int, dedup: b
     if parts:
         return {"stage_hbm": hbm, "nvl": nvl, "update_hbm": max(upd), "presum_hbm": max(pre),
                 "replicate_hbm": max(rep), "pcie_per_dir": 12 * E * Pg if host_state else 0,
-                "nvl_in": nin, "nvl_out": nout}
+                "nvl_in": nin, "nvl_out": nout, "update_per_gpu": upd, "presum_per_gpu": pre,
+                "replicate_per_gpu": rep}
     return hbm, nvl
 
 
@@ -792,6 +793,9 @@ def gpu_arm(args, wl):
         roof = {"kernel": kname + ", NVLink pulls/pushes", "bound": "nvlink",
                 "achieved": round(achieved, 1), "peak": GUIDE_NVLINK_GBS, "unit": "GB/s",
                 "frac": round(achieved / GUIDE_NVLINK_GBS, 4), "traffic": None,
+                "traffic_note": "ncu cannot replay this multi-rank kernel (in-kernel NVLink barriers, "
+                                "one process per GPU); the de-dup kernels' DRAM bytes are cross-checked "
+                                "in virtual mode instead: profiles/traffic.json 'gpt-small/G=4-virtual/*'",
                 "algorithmic_bytes_per_launch": int(mean["nvl"]),
                 "peak_source": "B200_PROFILING.md measured peer copy per direction (900 nominal)",
                 "avg_launch_ms": round(updk_avg, 4)}
