@@ -866,6 +866,97 @@ __global__ void __launch_bounds__(kThreads) k_presum(const __grid_constant__ Pre
   }
 }
 
+// k_presum_tma: the same partials (same bits) with the slices staged by bulk copies.  k_presum
+// keeps r x 16 B in flight per thread; in moe_step it runs as a persistent 2-CTA/SM grid (room
+// for the concurrent dispatch), so with r = 3 that is ~24 KB per SM -- latency-bound (0.77 of
+// the HBM peak even alone on the GPU).  Here one producer lane per CTA walks the CTA's items
+// (row, chunk) and their slices in the consumers' order and streams each 4 KB slice-chunk into
+// a kPreSlots-deep shared-memory ring (cp.async.bulk + mbarrier complete_tx): up to 64 KB in
+// flight per CTA at ~40 registers.  Consumers (8 warps) use the update kernel's two-group
+// element mapping (thread t: elements [4t, 4t+4) and [H+4t, H+4t+4) of the chunk), so every
+// fp32 warp store is one full 512-byte run.
+constexpr int kPreSlots = 16;
+constexpr size_t kPreSmem = (size_t)kPreSlots * kChunk * 2 + 2 * kPreSlots * 8;
+
+__global__ void __launch_bounds__(kTmaThreads) k_presum_tma(const __grid_constant__ PresumArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint16_t *ring = reinterpret_cast<uint16_t *>(smem);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)kPreSlots * kChunk * 2);
+  uint64_t *empty = full + kPreSlots;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kPreSlots; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t total = (int64_t)a.nq_total * a.nchunks;
+  constexpr int H = kChunk / 2;
+  uint32_t gi = 0;
+  if (warp == kConsumerWarps) {  // ---------------- producer ----------------
+    if (lane != 0) return;
+    for (int64_t it = blockIdx.x; it < total; it += gridDim.x) {
+      const int row = (int)(it / a.nchunks);
+      const int64_t c = it - (int64_t)row * a.nchunks;
+      int v = 0;
+      while (row >= a.qoff[v + 1]) ++v;
+      const int e = a.q_e[v][row - a.qoff[v]];
+      const int h = a.o_begin + v;
+      // the GPU's own owner range is never read as a partial (its owner reads the local slices
+      // directly, the same bits by A11): skip chunks entirely inside [h*Pg, (h+1)*Pg)
+      if (c * kChunk >= (int64_t)h * a.Pg && (c + 1) * kChunk <= (int64_t)(h + 1) * a.Pg) continue;
+      const uint32_t nval = (uint32_t)(a.P - c * kChunk < kChunk ? a.P - c * kChunk : kChunk);
+      const int ja = max(a.fs[e], h * a.S), jb = min(a.fs[e + 1], (h + 1) * a.S);
+      const uint16_t *src = a.grads[v] + c * kChunk;
+      for (int j = ja; j < jb; ++j, ++gi) {
+        const int g = gi % kPreSlots;
+        mbar_wait(empty + g, ((gi / kPreSlots) & 1) ^ 1);
+        mbar_expect_tx(full + g, nval * 2);
+        bulk_g2s(ring + (size_t)g * kChunk, src + (int64_t)(j - h * a.S) * a.P, nval * 2, full + g);
+      }
+    }
+    return;
+  }
+  // ---------------- consumers ----------------
+  const int tid = threadIdx.x;
+  for (int64_t it = blockIdx.x; it < total; it += gridDim.x) {
+    const int row = (int)(it / a.nchunks);
+    const int64_t c = it - (int64_t)row * a.nchunks;
+    int v = 0;
+    while (row >= a.qoff[v + 1]) ++v;
+    const int q = row - a.qoff[v];
+    const int e = a.q_e[v][q];
+    const int h = a.o_begin + v;
+    if (c * kChunk >= (int64_t)h * a.Pg && (c + 1) * kChunk <= (int64_t)(h + 1) * a.Pg) continue;
+    const int ja = max(a.fs[e], h * a.S), jb = min(a.fs[e + 1], (h + 1) * a.S);
+    float part[8];
+    for (int j = ja; j < jb; ++j, ++gi) {  // ascending slot order (reading A11)
+      const int g = gi % kPreSlots;
+      mbar_wait(full + g, (gi / kPreSlots) & 1);
+      const uint16_t *gs = ring + (size_t)g * kChunk + tid * 4;
+      const uint2 xa = *reinterpret_cast<const uint2 *>(gs);
+      const uint2 xb = *reinterpret_cast<const uint2 *>(gs + H);
+      release_slot(empty + g, lane);
+      float g8[8];
+      unpack_bf16x8(make_uint4(xa.x, xa.y, xb.x, xb.y), g8);
+      if (j == ja) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) part[k] = g8[k];
+      } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) part[k] = __fadd_rn(part[k], g8[k]);
+      }
+    }
+    // (lanes of a ragged last chunk computed on stale ring bytes and store nothing)
+    const int64_t loc = c * kChunk + (int64_t)tid * 4;
+    float *dst = a.presum[v] + (int64_t)q * a.P + loc;
+    if (loc < a.P) *reinterpret_cast<float4 *>(dst) = make_float4(part[0], part[1], part[2], part[3]);
+    if (loc + H < a.P) *reinterpret_cast<float4 *>(dst + H) = make_float4(part[4], part[5], part[6], part[7]);
+  }
+}
+
 struct ReplArgs {
   int32_t E, S, o_begin;
   int64_t P, Pg;
@@ -959,6 +1050,8 @@ int moe_update_init() {
   if (cudaFuncSetAttribute(k_update_tma<kGradSlots>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            tma_smem<kGradSlots>()) != cudaSuccess)
     return -1;
+  if (cudaFuncSetAttribute(k_presum_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPreSmem) != cudaSuccess)
+    return -1;
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_update, kThreads, 0) != cudaSuccess) return -1;
   return std::max(1, n);
@@ -999,6 +1092,13 @@ int build_presum(moe_ctx *ctx, const moe_plan_t *plan_cur, int8_t (&pq)[MOE_MAX_
     pa.presum[v] = ctx->presum[v];
   }
   return MOE_OK;
+}
+
+// The de-dup pre-sum launch: the bulk-copy kernel, or (MOE_PRESUM_KERNEL=ldg, A/B, read per
+// call) the register-staged k_presum.  Same partials, same bits.
+void launch_presum(int64_t grid, const PresumArgs &pa, cudaStream_t s) {
+  if (getenv("MOE_PRESUM_KERNEL") != nullptr) k_presum<<<(unsigned)grid, kThreads, 0, s>>>(pa);
+  else k_presum_tma<<<(unsigned)grid, kTmaThreads, kPreSmem, s>>>(pa);
 }
 
 // De-dup pre-sum inside the update kernel: opt-in (MOE_PRESUM_FUSED=1, read per call so tests
@@ -1141,7 +1241,7 @@ int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *pl
     } else if (pa.nq_total > 0) {
       const int64_t grid = std::min<int64_t>((int64_t)pa.nq_total * pa.nchunks, (int64_t)ctx->num_sms * 8);
       const auto pev = timing_begin(ctx, s);
-      k_presum<<<(unsigned)grid, kThreads, 0, s>>>(pa);
+      launch_presum(grid, pa, s);
       MOE_CUDA_TRY(cudaGetLastError());
       timing_end(ctx->ev_presum, pev, s);
     }
@@ -1380,7 +1480,7 @@ int moe_presum_prelaunch(moe_ctx *ctx, const moe_plan_t *plan_cur, void *stream)
                                            per_item ? ((int64_t)1 << 30) : (int64_t)ctx->num_sms * 2);
     const auto pev = timing_begin(ctx, ctx->side);
     tl_mark(ctx, TL_PRESUM_B, ctx->side);
-    k_presum<<<(unsigned)grid, kThreads, 0, ctx->side>>>(pa);
+    launch_presum(grid, pa, ctx->side);
     MOE_CUDA_TRY(cudaGetLastError());
     timing_end(ctx->ev_presum, pev, ctx->side);
     tl_mark(ctx, TL_PRESUM_E, ctx->side);
