@@ -965,13 +965,32 @@ struct ReplArgs {
   const int32_t *fs_dev;      // early launch: plan_next in device memory (valid iff *pflag == pepoch)
   const uint32_t *pflag;
   uint32_t pepoch;
+  // plan_next known on the host: a 1-D grid, CTAs given to each source (first local slot of an
+  // expert with local duplicates) in proportion to its bytes, (1 + ndup) x 2(P - Pg) -- one CTA
+  // row per slot gave a hot expert's 15 duplicates as few CTAs as a 1-duplicate expert, so its
+  // writes formed a long low-occupancy tail.  nsrc = 0: the 2-D grid (early launch).
+  int32_t nsrc;
+  int16_t src_slot[MOE_MAX_G * MOE_MAX_E];  // local rank v * S + slot l of source k  (S <= MOE_MAX_E)
+  int32_t cta_pre[MOE_MAX_G * MOE_MAX_E + 1];
 };
 
 // One CTA row per local slot; only the FIRST slot of an expert with local duplicates works: it
 // reads the remote owners' ranges of that slot once and stores them into every other local
 // slot of the expert (earlier version: one row per duplicate, re-reading the source each time).
 __global__ void __launch_bounds__(kThreads) k_replicate(const __grid_constant__ ReplArgs a) {
-  const int v = blockIdx.y / a.S, l = blockIdx.y % a.S;
+  int row = blockIdx.y, cb = blockIdx.x, ncb = gridDim.x;
+  if (a.nsrc > 0) {  // byte-weighted 1-D grid: source k owns CTAs [cta_pre[k], cta_pre[k+1])
+    int lo = 0, hi = a.nsrc - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (a.cta_pre[mid] <= (int)blockIdx.x) lo = mid;
+      else hi = mid - 1;
+    }
+    row = a.src_slot[lo];
+    cb = (int)blockIdx.x - a.cta_pre[lo];
+    ncb = a.cta_pre[lo + 1] - a.cta_pre[lo];
+  }
+  const int v = row / a.S, l = row % a.S;
   const int h = a.o_begin + v;
   const int j = h * a.S + l;
   const int32_t *fs = a.fs;
@@ -993,8 +1012,8 @@ __global__ void __launch_bounds__(kThreads) k_replicate(const __grid_constant__ 
   uint16_t *dst0 = a.w[v] + (int64_t)(l + 1) * a.P;
   const int64_t nrem = a.P - a.Pg, own = (int64_t)h * a.Pg;  // remote owners' elements
   constexpr int kU = 4;  // 16-byte vectors in flight per thread
-  const int64_t stride = (int64_t)gridDim.x * kThreads * kVec;
-  for (int64_t r0 = ((int64_t)blockIdx.x * kThreads + threadIdx.x) * kVec; r0 < nrem; r0 += kU * stride) {
+  const int64_t stride = (int64_t)ncb * kThreads * kVec;
+  for (int64_t r0 = ((int64_t)cb * kThreads + threadIdx.x) * kVec; r0 < nrem; r0 += kU * stride) {
     uint4 buf[kU];
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
@@ -1402,17 +1421,34 @@ int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *pl
       nsrc = std::max(1, ctx->n_local * ctx->S / 2);
     } else {
       for (int e = 0; e <= ctx->E; ++e) ra.fs[e] = plan_next->first_slot[e];
+      int64_t units = 0;  // (1 + ndup) summed over the sources
+      int ndup[MOE_MAX_G * MOE_MAX_E];
       for (int v = 0; v < ctx->n_local; ++v) {
         const int h = a.o_begin + v;
         for (int e = 0; e < ctx->E; ++e) {
           const int ja = std::max(ra.fs[e], h * ctx->S), jb = std::min(ra.fs[e + 1], (h + 1) * ctx->S);
-          if (jb - ja > 1) ++nsrc;
+          if (jb - ja > 1) {
+            ra.src_slot[nsrc] = (int16_t)(v * ctx->S + (ja - h * ctx->S));
+            ndup[nsrc] = jb - ja - 1;
+            units += jb - ja;
+            ++nsrc;
+          }
         }
       }
+      // ~8 CTAs per SM in all, each source at least one and at most one per 8 K-element unit
+      const int64_t cap = (ctx->P - ctx->Pg) / (kThreads * kVec) + 1;
+      const int64_t budget = 8 * (int64_t)ctx->num_sms;
+      ra.cta_pre[0] = 0;
+      for (int k = 0; k < nsrc; ++k) {
+        const int64_t want = std::max<int64_t>(1, std::min<int64_t>(cap, budget * (1 + ndup[k]) / std::max<int64_t>(1, units)));
+        ra.cta_pre[k + 1] = ra.cta_pre[k] + (int32_t)want;
+      }
+      ra.nsrc = getenv("MOE_REPL_GRID") ? 0 : nsrc;  // A/B (read per call): the 2-D one-row-per-slot grid
     }
     if (nsrc > 0) {
-      const int gx = std::max(1, std::min<int>((int)((ctx->P - ctx->Pg) / (kThreads * kVec)) + 1,
-                                               8 * ctx->num_sms / nsrc + 1));
+      const int gx = ra.nsrc > 0 ? ra.cta_pre[ra.nsrc]
+                                 : std::max(1, std::min<int>((int)((ctx->P - ctx->Pg) / (kThreads * kVec)) + 1,
+                                                             8 * ctx->num_sms / nsrc + 1));
       cudaStream_t rs = s;
       if (ctx->lazy_repl) {  // off the caller's stream; joined before the next slot-weight writer
         MOE_CUDA_TRY(cudaEventRecord(ctx->ev_repl_in, s));
@@ -1421,7 +1457,7 @@ int launch_update(moe_ctx *ctx, const moe_plan_t *plan_cur, const moe_plan_t *pl
       }
       const auto rev = timing_begin(ctx, rs);
       tl_mark(ctx, TL_REPL_B, rs);
-      k_replicate<<<dim3(gx, ctx->n_local * ctx->S), kThreads, 0, rs>>>(ra);
+      k_replicate<<<dim3(gx, ra.nsrc > 0 ? 1 : ctx->n_local * ctx->S), kThreads, 0, rs>>>(ra);
       MOE_CUDA_TRY(cudaGetLastError());
       timing_end(ctx->ev_repl, rev, rs);
       tl_mark(ctx, TL_REPL_E, rs);

@@ -1,4 +1,5 @@
-"""A/B of the de-dup pre-sum kernels in virtual mode on one GPU (development tool): the bulk-copy
+"""A/B of the de-dup pre-sum kernels (and of k_replicate's byte-weighted grid vs the 2-D
+one-row-per-slot grid, MOE_REPL_GRID=rows, in the "ldg" arm) in virtual mode on one GPU (development tool): the bulk-copy
 k_presum_tma (default) vs the register-staged k_presum (MOE_PRESUM_KERNEL=ldg, read per call),
 through moe_step (the persistent 2-CTA/SM pre-sum grid on the side stream) and through
 moe_update (the 8-CTA/SM grid).  Library CUDA events; algorithmic bytes from
@@ -32,16 +33,18 @@ def main(name="gpt-small", G=4, iters=12):
     dev = [(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()) for a, b in tr]
     res = {"config": name, "G": G, "mode": "virtual (one GPU)"}
     for kern in ("tma", "ldg", "tma", "ldg"):
-        if kern == "ldg":
+        if kern == "ldg":  # also the 2-D replicate grid (MOE_REPL_GRID) in the same arm
             os.environ["MOE_PRESUM_KERNEL"] = "ldg"
+            os.environ["MOE_REPL_GRID"] = "rows"
         else:
             os.environ.pop("MOE_PRESUM_KERNEL", None)
+            os.environ.pop("MOE_REPL_GRID", None)
         for path in ("step", "update"):
             layer.iterate(*dev[0], Tg)
             torch.cuda.synchronize()
             layer.ctx.get_timing()
             layer.ctx.set_timing(True)
-            byts = 0
+            byts = rbyts = 0
             for i in range(1, iters):
                 cur = layer.plan.first_slot.copy()
                 if path == "step":
@@ -52,12 +55,16 @@ def main(name="gpt-small", G=4, iters=12):
                     layer.update(nxt)
                 b = bench.update_stage_bytes(cur, nxt.first_slot, G, S, wl.P, wl.E, True, parts=True)
                 byts += sum(b["presum_per_gpu"])
+                rbyts += sum(b["replicate_per_gpu"])
             torch.cuda.synchronize()
             tm = layer.ctx.get_timing()
             layer.ctx.set_timing(False)
             ms = tm["presum_ms"] / max(1, tm["n_presum"])
             gbs = byts / max(1, tm["n_presum"]) / (ms * 1e-3) / 1e9
+            rms = tm["replicate_ms"] / max(1, tm["n_replicate"])
+            rgbs = rbyts / max(1, tm["n_replicate"]) / (rms * 1e-3) / 1e9
             res[f"{kern}/{path}"] = {"presum_ms": round(ms, 4), "GB/s": round(gbs, 1), "n": tm["n_presum"],
+                                     "replicate_ms": round(rms, 4), "replicate_GB/s": round(rgbs, 1),
                                      "update_kernel_ms": round(tm["update_kernel_ms"] / max(1, tm["n_update_kernel"]), 4)}
             print(kern, path, res[f"{kern}/{path}"], flush=True)
     print(json.dumps(res))
